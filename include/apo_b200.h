@@ -1,0 +1,156 @@
+/*
+ * apo_b200.h -- C ABI of libapo_b200.so, the B200 (sm_100a) APO hot path.
+ *
+ * The drop-in boundary is the reference's backend plug-in protocol
+ * (/root/reference/pkg/src/protozoa/kernels/__init__.py:47-56): a backend
+ * module exposes NAME, max_workers() and run_updates(...).  The reference's
+ * only compiled code is the numba dispatcher that run_updates calls
+ * (kernels/numba_backend.py:367-371, `_step_parallel(*args)` with the flat
+ * argument tuple built at :425-433); apo_run_updates() below takes exactly
+ * that tuple, as device pointers, plus sizes and a stream.  The Python
+ * backend paper_2510_14982_b200/kernels/cuda_backend.py binds it with
+ * ctypes (see INTEGRATION.md for the binding a reference maintainer adds).
+ *
+ * Conventions
+ *  - every pointer argument is a DEVICE pointer unless the parameter name
+ *    ends in _host;
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream);
+ *  - every function returns 0 on success, or a nonzero status whose text is
+ *    available from apo_last_error() (thread-local); invalid arguments are
+ *    rejected with APO_EINVAL before any launch;
+ *  - no function reads or writes its input population (numba_backend.py
+ *    :401-404 "Inputs are read only"); callers own all outputs.
+ */
+#ifndef APO_B200_H
+#define APO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APO_OK 0
+#define APO_EINVAL 1
+#define APO_ECUDA 2
+#define APO_ENOMEM 3
+
+/* Objective codes (objectives.py:34-42), plus codes the reference lacks. */
+#define APO_OBJ_SPHERE 0
+#define APO_OBJ_BENT_CIGAR 1
+#define APO_OBJ_ELLIPTIC 2 /* table = elliptic weights (objectives.py:88-102) */
+#define APO_OBJ_HGBAT 3
+#define APO_OBJ_ROSENBROCK 4
+#define APO_OBJ_GRIEWANK 5
+#define APO_OBJ_TABLE 6 /* table[round_half_up(x0)] (objectives.py:183-192, 213-219) */
+
+/* An objective as the kernels see it (device pointers). */
+typedef struct apo_objective {
+    int32_t code;
+    int32_t table_len;
+    const double *table;
+} apo_objective;
+
+int apo_abi_version(void);
+const char *apo_last_error(void);
+/* Number of visible CUDA devices (cuda backend max_workers()). */
+int apo_device_count(void);
+
+/*
+ * One iteration's per-individual phase over a rank-sorted snapshot.
+ * Replaces numba_backend.run_updates (kernels/numba_backend.py:323-372):
+ * same inputs (positions [ps, dim] row-major, rank r+1 in row r; fitness
+ * [ps]; in_dr [ps] bool by rank), same flat scalars (:425-433), same
+ * outputs (new positions/fitness in rank order, accepted, warned).
+ * p_dr [ps] holds 0.5*(1-cos((1-i/ps)*pi)) per rank (numba_backend.py:
+ * 173-175), computed by the host with libm so the decision threshold is
+ * bit-identical; warn_count (nullable) receives the number of warned rows.
+ */
+int apo_run_updates(const double *positions, const double *fitness, const uint8_t *in_dr, double *out_pos,
+                    double *out_fit, uint8_t *out_acc, uint8_t *out_warn, int64_t ps, int64_t dim, uint64_t seed,
+                    uint64_t key_iteration, int64_t npairs, double lower, double upper, double span, double eps,
+                    double p_ah, double f_mult, double decay, int64_t code, const double *table, int64_t table_len,
+                    const double *p_dr, unsigned long long *warn_count, void *stream);
+
+/* Same, for any objective descriptor (codes the reference does not have). */
+int apo_run_updates_obj(const double *positions, const double *fitness, const uint8_t *in_dr, double *out_pos,
+                        double *out_fit, uint8_t *out_acc, uint8_t *out_warn, int64_t ps, int64_t dim, uint64_t seed,
+                        uint64_t key_iteration, int64_t npairs, double lower, double upper, double eps, double p_ah,
+                        double f_mult, double decay, const apo_objective *objective_host, const double *p_dr,
+                        unsigned long long *warn_count, void *stream);
+
+/* Batch fitness: out[r] = f(x[r*ld .. r*ld+dim)) (objectives.evaluate_unchecked,
+ * objectives.py:222-228). */
+int apo_evaluate(const double *x, int64_t n, int64_t dim, int64_t ld, const apo_objective *objective_host, double *out,
+                 void *stream);
+
+/* Iteration-0 population (engine.initialize, engine.py:116-139): row s =
+ * lower + u(seed, 0, s+1, d) * span, then its fitness. */
+int apo_initialize(uint64_t seed, int64_t ps, int64_t dim, int64_t ld, double lower, double span,
+                   const apo_objective *objective_host, double *positions, double *fitness, void *stream);
+
+/* Stable ascending argsort of fitness (core.sort_by_fitness, core.py:
+ * 504-513): order[r] = row holding rank r+1; ties keep row order,
+ * -0.0 == +0.0, NaN last. */
+int apo_sort_order(const double *fitness, int64_t n, int32_t *order, void *stream);
+
+/* Coordinator draws (core.py:263-278, engine.py:157-162): in_dr[r] = 1 iff
+ * rank r+1 is in this iteration's dormancy/reproduction set.  Returns the
+ * set size through count_host (nullable). */
+int apo_select_dr(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_max, uint8_t *in_dr,
+                  int64_t *count_host, void *stream);
+
+/* 256-bin histogram of an 8-bit image (imaging.histogram, imaging.py:197-200). */
+int apo_histogram_u8(const uint8_t *pixels, int64_t n, int64_t *counts, void *stream);
+
+/*
+ * Device-resident run (engine.run, engine.py:175-212).  The population
+ * stays in HBM in slot order; each iteration is a stable key sort (rank ->
+ * slot order, no row gather), the coordinator draws and one fused update
+ * launch.  sched_host: [max_iterations][3] = (p_ah, f_mult, decay) per
+ * iteration; p_dr_host: [ps].  Both are computed by the host with libm
+ * exactly as numba_backend.py:357-366 and :173-175 do.
+ */
+typedef struct apo_run apo_run;
+int apo_run_create(apo_run **out, int64_t ps, int64_t dim, int64_t max_iterations, uint64_t seed, int64_t npairs,
+                   double pf_max, double lower, double upper, double eps, const apo_objective *objective_host,
+                   const double *sched_host, const double *p_dr_host, void *stream);
+int apo_run_initialize(apo_run *run);
+/* Runs iterations [t, t+n) where t is the number already run. */
+int apo_run_iterate(apo_run *run, int64_t n);
+/* Trace entries 0..iterations_run as doubles (host buffer of >= n+1). */
+int apo_run_trace(apo_run *run, double *trace_host, int64_t n);
+/* Current population in reference row order (row r = rank r+1 of the last
+ * snapshot, i.e. what engine.step returns), device or host buffers. */
+int apo_run_population(apo_run *run, double *positions, double *fitness, int is_host);
+/* Best individual (Population.best, core.py:195-196: first argmin in
+ * reference row order). */
+int apo_run_best(apo_run *run, double *best_fitness_host, double *best_position_host, int64_t *best_row_host);
+int apo_run_counters(apo_run *run, int64_t *iterations_run, int64_t *fe_count, int64_t *warnings);
+int apo_run_destroy(apo_run *run);
+
+/*
+ * Many independent small runs, one CTA per run, the whole run resident in
+ * shared memory for all iterations (BASELINE configs 1-3 and 5: seeds x
+ * objectives).  objectives_host: nruns descriptors; seeds: device [nruns].
+ * Outputs (device, nullable except best_fit): best_fit [nruns], best_pos
+ * [nruns, dim], trace [nruns, n_iters+1], final_pos [nruns, ps, dim] and
+ * final_fit [nruns, ps] in reference row order, warnings [nruns].
+ * n_iters <= max_iterations is the number of iterations actually run
+ * (max_fes budget, engine.py:192-193).
+ */
+int apo_run_batch(int64_t nruns, const uint64_t *seeds, const apo_objective *objectives_host, int64_t ps,
+                  int64_t dim, int64_t max_iterations, int64_t n_iters, int64_t npairs, double pf_max, double lower,
+                  double upper, double eps, const double *sched, const double *p_dr, double *best_fit,
+                  double *best_pos, double *trace, double *final_pos, double *final_fit, int64_t *warnings,
+                  void *stream);
+/* Largest ps*dim the batch kernel can hold in shared memory. */
+int64_t apo_run_batch_max_elems(int64_t ps, int64_t dim);
+
+/* Debug/verification entry: out[k] = device exp_glibc(x[k]). */
+int apo_debug_exp(const double *x, double *out, int64_t n, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APO_B200_H */

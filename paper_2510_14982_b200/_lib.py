@@ -1,0 +1,152 @@
+"""Loader and builder for libapo_b200.so (the sm_100a kernels behind the C ABI).
+
+The library is built in-tree with nvcc (``build()``), loaded with ctypes
+and bound to the prototypes of include/apo_b200.h.  There is no CPU
+fallback: if the library is missing or a CUDA device is absent, every entry
+point raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import shutil
+import subprocess
+import threading
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG_DIR)
+CSRC = os.path.join(PKG_DIR, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB_PATH = os.path.join(PKG_DIR, "libapo_b200.so")
+
+ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# --fmad=false: oracle-exact arithmetic (the reference never fuses mul+add).
+NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+              "-diag-suppress", "177"]
+SOURCES = ["apo_kernels.cu"]
+
+_lock = threading.Lock()
+_lib = None
+
+
+class ApoError(RuntimeError):
+    """A C-ABI call failed (CUDA error or rejected argument)."""
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise ApoError("nvcc not found; cannot build libapo_b200.so")
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB_PATH):
+        return True
+    t = os.path.getmtime(LIB_PATH)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "apo_b200.h")]
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libapo_b200.so for sm_100a (in-tree, so it travels with the repo)."""
+    with _lock:
+        if not force and not _stale():
+            return LIB_PATH
+        tmp = LIB_PATH + ".tmp"
+        cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp,
+               *[os.path.join(CSRC, s) for s in SOURCES]]
+        if verbose:
+            print(" ".join(cmd))
+        proc = subprocess.run(cmd, capture_output=True, text=True)
+        if proc.returncode != 0:
+            raise ApoError(f"nvcc failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
+        os.replace(tmp, LIB_PATH)
+        return LIB_PATH
+
+
+_P = C.c_void_p
+_I = C.c_int64
+_U = C.c_uint64
+_D = C.c_double
+_INT = C.c_int
+
+
+class apo_objective(C.Structure):
+    _fields_ = [("code", C.c_int32), ("table_len", C.c_int32), ("table", C.c_void_p)]
+
+
+PROTOTYPES = {
+    "apo_abi_version": (_INT, []),
+    "apo_last_error": (C.c_char_p, []),
+    "apo_device_count": (_INT, []),
+    "apo_run_updates": (_INT, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _U, _U, _I, _D, _D, _D, _D, _D, _D, _D, _I, _P,
+                               _I, _P, _P, _P]),
+    "apo_run_updates_obj": (_INT, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _U, _U, _I, _D, _D, _D, _D, _D, _D,
+                                   C.POINTER(apo_objective), _P, _P, _P]),
+    "apo_evaluate": (_INT, [_P, _I, _I, _I, C.POINTER(apo_objective), _P, _P]),
+    "apo_initialize": (_INT, [_U, _I, _I, _I, _D, _D, C.POINTER(apo_objective), _P, _P, _P]),
+    "apo_sort_order": (_INT, [_P, _I, _P, _P]),
+    "apo_select_dr": (_INT, [_U, _U, _I, _D, _P, C.POINTER(C.c_int64), _P]),
+    "apo_histogram_u8": (_INT, [_P, _I, _P, _P]),
+    "apo_run_create": (_INT, [C.POINTER(C.c_void_p), _I, _I, _I, _U, _I, _D, _D, _D, _D, C.POINTER(apo_objective),
+                              _P, _P, _P]),
+    "apo_run_initialize": (_INT, [_P]),
+    "apo_run_iterate": (_INT, [_P, _I]),
+    "apo_run_trace": (_INT, [_P, _P, _I]),
+    "apo_run_population": (_INT, [_P, _P, _P, _INT]),
+    "apo_run_best": (_INT, [_P, _P, _P, C.POINTER(C.c_int64)]),
+    "apo_run_counters": (_INT, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "apo_run_destroy": (_INT, [_P]),
+    "apo_run_batch": (_INT, [_I, _P, C.POINTER(apo_objective), _I, _I, _I, _I, _I, _D, _D, _D, _D, _P, _P, _P, _P,
+                             _P, _P, _P, _P, _P]),
+    "apo_run_batch_max_elems": (_I, [_I, _I]),
+    "apo_debug_exp": (_INT, [_P, _P, _I, _P]),
+}
+
+
+def load(path: str = LIB_PATH):
+    """dlopen the library and bind every prototype (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ApoError(f"{path} is missing: run __graft_entry__.build() (or paper_2510_14982_b200._lib.build())")
+        lib = C.CDLL(path)
+        for name, (res, args) in PROTOTYPES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = load().apo_last_error().decode(errors="replace")
+        raise ApoError(f"{what or 'libapo_b200'} failed (status {rc}): {msg}")
+
+
+def require_cuda():
+    """The CUDA path is the only path: fail loudly without a device."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise ApoError("the cuda backend needs a CUDA device (no CPU fallback exists)")
+    return load()
+
+
+def stream_handle(stream=None) -> C.c_void_p:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def ptr(t) -> C.c_void_p:
+    """Device pointer of a CUDA tensor (None -> NULL)."""
+    if t is None:
+        return C.c_void_p(0)
+    return C.c_void_p(t.data_ptr())

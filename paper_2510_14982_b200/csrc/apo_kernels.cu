@@ -1,0 +1,1033 @@
+// apo_kernels.cu -- sm_100a kernels and the C ABI of libapo_b200.so.
+//
+// Built with --fmad=false (oracle-exact arithmetic).
+// Kernels:
+//   k_update<INDIRECT>  fused per-protozoon update, one warp per protozoon
+//                       (numba_backend.py:141-290); dense rank-ordered rows
+//                       at the run_updates boundary, or slot-resident rows
+//                       through the rank->slot order in the device loop.
+//                       Fuses the best-so-far min (engine.py:196) and the
+//                       warning count (numba_backend.py:372).
+//   k_init              iteration-0 draws + evaluation (engine.py:116-139)
+//   k_evaluate          batch fitness (objectives.py:222-228)
+//   k_make_keys         fitness -> order-preserving u64 keys for the stable
+//                       radix sort (core.py:504-513)
+//   k_dr_draw/resolve   coordinator Dr set (core.py:263-278) as a parallel
+//                       partial Fisher-Yates (see apo_update.cuh:build_mask)
+//   k_run_batch         persistent run: one CTA per independent run, the
+//                       population in shared memory for every iteration
+//   k_histogram_u8      shared-memory privatised 256-bin histogram
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "apo_b200.h"
+#include "apo_update.cuh"
+
+using namespace apo;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define APO_CUDA(call)                                                                             \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return fail(APO_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define APO_CHECK(cond, msg)                         \
+    do {                                             \
+        if (!(cond)) return fail(APO_EINVAL, (msg)); \
+    } while (0)
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// Warps per CTA for a given dim so the per-warp scratch fits comfortably.
+int warps_for_dim(int64_t dim) {
+    size_t per = warp_scratch_bytes((int)dim);
+    int w = kWarps;
+    while (w > 1 && per * (size_t)w > 96 * 1024) w >>= 1;
+    return w;
+}
+
+int set_smem(const void* fn, size_t bytes) {
+    if (bytes > 48 * 1024) APO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return APO_OK;
+}
+
+ObjDesc to_desc(const apo_objective* o) {
+    ObjDesc d;
+    d.code = o->code;
+    d.table_len = o->table_len;
+    d.table = o->table;
+    return d;
+}
+
+int check_objective(const apo_objective* o, int64_t dim) {
+    APO_CHECK(o != nullptr, "objective descriptor is NULL");
+    APO_CHECK(o->code >= APO_OBJ_SPHERE && o->code <= APO_OBJ_TABLE, "unsupported objective code");
+    if (o->code == APO_OBJ_ELLIPTIC) APO_CHECK(o->table && o->table_len >= dim, "elliptic needs dim weights");
+    if (o->code == APO_OBJ_TABLE) APO_CHECK(o->table && o->table_len >= 1, "table objective needs a table");
+    return APO_OK;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(kFull, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+template <bool INDIRECT>
+__global__ void __launch_bounds__(kThreads) k_update(IterParams P, ObjDesc O, const double* __restrict__ pos,
+                                                     const double* __restrict__ fit, const int* __restrict__ order,
+                                                     const uint8_t* __restrict__ in_dr_bytes,
+                                                     const unsigned* __restrict__ in_dr_bits,
+                                                     const double* __restrict__ p_dr, double* __restrict__ out_pos,
+                                                     double* __restrict__ out_fit, uint8_t* __restrict__ out_acc,
+                                                     uint8_t* __restrict__ out_warn,
+                                                     unsigned long long* __restrict__ warn_count,
+                                                     unsigned long long* __restrict__ trace_key) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long red_min[32];
+    __shared__ unsigned red_warn[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const WarpScratch s = warp_scratch(smem + (size_t)warp * warp_scratch_bytes(P.dim), P.dim);
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    for (int r0 = blockIdx.x * nwarps + warp; r0 < P.ps; r0 += gridDim.x * nwarps) {
+        const bool dr = in_dr_bits ? ((in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0 : in_dr_bytes[r0] != 0;
+        const double pdr = dr ? p_dr[r0] : 0.0;
+        UpdateResult res;
+        if (INDIRECT) {
+            const OrderedRows R{pos, fit, order, P.ld};
+            const int slot = order[r0];
+            res = update_protozoon(P, O, R, r0 + 1, dr, pdr, out_pos + (size_t)slot * P.ld, s, lane);
+            if (lane == 0) out_fit[slot] = res.fitness;
+        } else {
+            const DenseRows R{pos, fit, P.ld};
+            res = update_protozoon(P, O, R, r0 + 1, dr, pdr, out_pos + (size_t)r0 * P.ld, s, lane);
+            if (lane == 0) {
+                out_fit[r0] = res.fitness;
+                if (out_acc) out_acc[r0] = res.accepted ? 1 : 0;
+                if (out_warn) out_warn[r0] = res.warned ? 1 : 0;
+            }
+        }
+        const unsigned long long k = sort_key(res.fitness);
+        my_min = k < my_min ? k : my_min;
+        my_warn += res.warned ? 1u : 0u;
+    }
+    if (lane == 0) {
+        red_min[warp] = my_min;
+        red_warn[warp] = my_warn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = ~0ull;
+        unsigned w = 0;
+        for (int k = 0; k < nwarps; k++) {
+            m = red_min[k] < m ? red_min[k] : m;
+            w += red_warn[k];
+        }
+        if (trace_key && m != ~0ull) atomicMin(trace_key, m);
+        if (warn_count && w) atomicAdd(warn_count, (unsigned long long)w);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_init(uint64_t seed, int ps, int dim, int ld, double lower,
+                                                   double span, ObjDesc O, double* __restrict__ pos,
+                                                   double* __restrict__ fit, unsigned long long* trace_key) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long red_min[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const WarpScratch s = warp_scratch(smem + (size_t)warp * warp_scratch_bytes(dim), dim);
+    unsigned long long my_min = ~0ull;
+    for (int r0 = blockIdx.x * nwarps + warp; r0 < ps; r0 += gridDim.x * nwarps) {
+        const uint64_t base = stream_base(seed, 0, (uint64_t)(r0 + 1));
+        double* row = pos + (size_t)r0 * ld;
+        for (int d = lane; d < dim; d += 32) {
+            const double c = lower + uniform(base, (uint64_t)d) * span;
+            s.cand[d] = c;
+            row[d] = c;
+        }
+        __syncwarp();
+        const double f = eval_warp(O, s.cand, s.terms, dim, lane);
+        if (lane == 0) fit[r0] = f;
+        const unsigned long long k = sort_key(f);
+        my_min = k < my_min ? k : my_min;
+    }
+    if (lane == 0) red_min[warp] = my_min;
+    __syncthreads();
+    if (threadIdx.x == 0 && trace_key) {
+        unsigned long long m = ~0ull;
+        for (int k = 0; k < nwarps; k++) m = red_min[k] < m ? red_min[k] : m;
+        if (m != ~0ull) atomicMin(trace_key, m);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_evaluate(const double* __restrict__ x, int n, int dim, int ld, ObjDesc O,
+                                                       double* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const WarpScratch s = warp_scratch(smem + (size_t)warp * warp_scratch_bytes(dim), dim);
+    for (int r0 = blockIdx.x * nwarps + warp; r0 < n; r0 += gridDim.x * nwarps) {
+        const double* row = x + (size_t)r0 * ld;
+        for (int d = lane; d < dim; d += 32) s.cand[d] = row[d];
+        __syncwarp();
+        const double f = eval_warp(O, s.cand, s.terms, dim, lane);
+        if (lane == 0) out[r0] = f;
+    }
+}
+
+__global__ void k_make_keys(int n, const double* __restrict__ fit, const int* __restrict__ order,
+                            unsigned long long* __restrict__ keys, int* __restrict__ vals) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int slot = order ? order[r] : r;
+        keys[r] = sort_key(fit[slot]);
+        vals[r] = slot;
+    }
+}
+
+__global__ void k_iota(int n, int* __restrict__ v) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) v[r] = r;
+}
+
+// Coordinator Dr set, parallel partial Fisher-Yates (rng.py:137-156 on
+// counters 1.., core.py:271-278).  Step j's target r_j is packed with j so a
+// radix sort groups same-target steps in step order; resolution then walks
+// "latest earlier step with the same target" by binary search.
+__global__ void k_dr_draw(int count, int n, uint64_t base, unsigned long long* __restrict__ keys) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+        const double u = uniform(base, 1ull + (uint64_t)j);
+        int r = j + (int)(u * (double)(n - j));
+        if (r > n - 1) r = n - 1;
+        keys[j] = ((unsigned long long)r << 32) | (unsigned)j;
+    }
+}
+
+__device__ __forceinline__ int latest_before(const unsigned long long* keys, int count, unsigned p, unsigned t) {
+    // largest index q with keys[q] < (p<<32 | t); -1 if none or target differs
+    const unsigned long long probe = ((unsigned long long)p << 32) | t;
+    int lo = 0, hi = count;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < probe) lo = mid + 1;
+        else hi = mid;
+    }
+    const int q = lo - 1;
+    if (q < 0 || (unsigned)(keys[q] >> 32) != p) return -1;
+    return (int)(keys[q] & 0xFFFFFFFFull);
+}
+
+__global__ void k_dr_resolve(int count, int n, uint64_t base, const unsigned long long* __restrict__ keys,
+                             unsigned* __restrict__ bits, uint8_t* __restrict__ bytes) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+        const double u = uniform(base, 1ull + (uint64_t)j);
+        int p = j + (int)(u * (double)(n - j));
+        if (p > n - 1) p = n - 1;
+        int t = j;
+        for (;;) {
+            const int q = latest_before(keys, count, (unsigned)p, (unsigned)t);
+            if (q < 0) break;
+            p = q;
+            t = q;
+        }
+        if (bits) atomicOr(&bits[p >> 5], 1u << (p & 31));
+        if (bytes) bytes[p] = 1;
+    }
+}
+
+__global__ void k_gather_rows(int n, int dim, int ld, const double* __restrict__ pos, const double* __restrict__ fit,
+                              const int* __restrict__ order, double* __restrict__ out_pos,
+                              double* __restrict__ out_fit) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < n; r += nw) {
+        const int slot = order[r];
+        for (int d = lane; d < dim; d += 32) out_pos[(size_t)r * dim + d] = pos[(size_t)slot * ld + d];
+        if (lane == 0 && out_fit) out_fit[r] = fit[slot];
+    }
+}
+
+__global__ void k_histogram_u8(const uint8_t* __restrict__ px, long long n, unsigned long long* __restrict__ counts) {
+    __shared__ unsigned h[kWarps][256];
+    const int warp = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < kWarps * 256; k += blockDim.x) (&h[0][0])[k] = 0u;
+    __syncthreads();
+    const long long nvec = n / 16;
+    const uint4* v = reinterpret_cast<const uint4*>(px);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nvec;
+         q += (long long)gridDim.x * blockDim.x) {
+        const uint4 w = v[q];
+        const unsigned words[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int a = 0; a < 4; a++) {
+#pragma unroll
+            for (int b = 0; b < 4; b++) atomicAdd(&h[warp][(words[a] >> (8 * b)) & 0xFFu], 1u);
+        }
+    }
+    for (long long q = nvec * 16 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x)
+        atomicAdd(&h[warp][px[q]], 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+        unsigned long long s = 0;
+        for (int w = 0; w < kWarps; w++) s += h[w][b];
+        if (s) atomicAdd(&counts[b], s);
+    }
+}
+
+__global__ void k_debug_exp(const double* x, double* out, long long n) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        out[k] = exp_glibc(x[k]);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent batched runs: one CTA = one independent run, resident in SMEM.
+struct BatchArgs {
+    const uint64_t* seeds;
+    const ObjDesc* objs;
+    int ps, dim, ld, max_iterations, n_iters, npairs;
+    double pf_max, lower, upper, span, eps;
+    const double* sched;  // [max_iterations][3]
+    const double* p_dr;   // [ps]
+    double* best_fit;
+    double* best_pos;
+    double* trace;
+    double* final_pos;
+    double* final_fit;
+    long long* warnings;
+};
+
+struct BatchLayout {
+    size_t pos0, pos1, fit0, fit1, keys, order, rankof, newrank, chead, cprev, crj, cbits, warps, total;
+};
+
+__host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int nwarps) {
+    BatchLayout L;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o += (bytes + 15) & ~(size_t)15;
+        return at;
+    };
+    L.pos0 = take(8 * (size_t)ps * ld);
+    L.pos1 = take(8 * (size_t)ps * ld);
+    L.fit0 = take(8 * (size_t)ps);
+    L.fit1 = take(8 * (size_t)ps);
+    L.keys = take(8 * (size_t)ps);
+    L.order = take(4 * (size_t)ps);
+    L.rankof = take(4 * (size_t)ps);
+    L.newrank = take(4 * (size_t)ps);
+    L.chead = take(4 * (size_t)ps);
+    L.cprev = take(4 * (size_t)ps);
+    L.crj = take(4 * (size_t)ps);
+    L.cbits = take(4 * (size_t)((ps + 31) / 32));
+    L.warps = take(warp_scratch_bytes(dim) * (size_t)nwarps);
+    L.total = o;
+    return L;
+}
+
+__global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long red_min[32];
+    __shared__ unsigned red_warn[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int run = blockIdx.x;
+    const int ps = A.ps, dim = A.dim, ld = A.ld;
+    const BatchLayout L = batch_layout(ps, dim, ld, nwarps);
+    double* pos[2] = {reinterpret_cast<double*>(smem + L.pos0), reinterpret_cast<double*>(smem + L.pos1)};
+    double* fit[2] = {reinterpret_cast<double*>(smem + L.fit0), reinterpret_cast<double*>(smem + L.fit1)};
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + L.keys);
+    int* order = reinterpret_cast<int*>(smem + L.order);
+    int* rankof = reinterpret_cast<int*>(smem + L.rankof);
+    int* newrank = reinterpret_cast<int*>(smem + L.newrank);
+    WarpScratch cs;
+    cs.head = reinterpret_cast<int*>(smem + L.chead);
+    cs.prev = reinterpret_cast<int*>(smem + L.cprev);
+    cs.rj = reinterpret_cast<int*>(smem + L.crj);
+    cs.bits = reinterpret_cast<unsigned*>(smem + L.cbits);
+    const WarpScratch ws = warp_scratch(smem + L.warps + (size_t)warp * warp_scratch_bytes(dim), dim);
+    const uint64_t seed = A.seeds[run];
+    const ObjDesc O = A.objs[run];
+    double* trace = A.trace ? A.trace + (size_t)run * (A.n_iters + 1) : nullptr;
+
+    // initialisation (engine.py:116-139)
+    unsigned long long my_min = ~0ull;
+    for (int r0 = warp; r0 < ps; r0 += nwarps) {
+        const uint64_t base = stream_base(seed, 0, (uint64_t)(r0 + 1));
+        double* row = pos[0] + (size_t)r0 * ld;
+        for (int d = lane; d < dim; d += 32) row[d] = A.lower + uniform(base, (uint64_t)d) * A.span;
+        __syncwarp();
+        for (int d = lane; d < dim; d += 32) ws.cand[d] = row[d];
+        __syncwarp();
+        const double f = eval_warp(O, ws.cand, ws.terms, dim, lane);
+        if (lane == 0) {
+            fit[0][r0] = f;
+            keys[r0] = sort_key(f);
+            order[r0] = r0;
+            rankof[r0] = r0;
+            my_min = sort_key(f) < my_min ? sort_key(f) : my_min;
+        }
+    }
+    if (lane == 0) red_min[warp] = my_min;
+    __syncthreads();
+    if (threadIdx.x == 0 && trace) {
+        unsigned long long m = ~0ull;
+        for (int k = 0; k < nwarps; k++) m = red_min[k] < m ? red_min[k] : m;
+        trace[0] = key_to_double(m);
+    }
+    unsigned warn_total = 0;
+    int cur = 0;
+    for (int t = 0; t < A.n_iters; t++) {
+        // 1. stable sort by fitness, ties by previous rank (core.py:504-513)
+        for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) {
+            const unsigned long long k = keys[sl];
+            const int pr = rankof[sl];
+            int cnt = 0;
+            for (int q = 0; q < ps; q++) {
+                const unsigned long long kq = keys[q];
+                cnt += (kq < k) || (kq == k && rankof[q] < pr);
+            }
+            newrank[sl] = cnt;
+        }
+        __syncthreads();
+        for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) {
+            order[newrank[sl]] = sl;
+            rankof[sl] = newrank[sl];
+        }
+        // 2. coordinator draws (core.py:263-278)
+        const uint64_t key_it = (uint64_t)t + 1;
+        if (warp == 0) {
+            const uint64_t cbase = stream_base(seed, key_it, kCoordinator);
+            const double pf = A.pf_max * uniform(cbase, 0);
+            const int count = (int)ceil((double)ps * pf);
+            build_mask(ps, count, cbase, 1, cs, lane);
+        }
+        __syncthreads();
+        // 3. fused updates
+        IterParams P;
+        P.seed = seed;
+        P.key_iteration = key_it;
+        P.ps = ps;
+        P.dim = dim;
+        P.npairs = A.npairs;
+        P.ld = ld;
+        P.lower = A.lower;
+        P.upper = A.upper;
+        P.span = A.span;
+        P.eps = A.eps;
+        P.p_ah = A.sched[3 * t];
+        P.f_mult = A.sched[3 * t + 1];
+        P.decay = A.sched[3 * t + 2];
+        const OrderedRows R{pos[cur], fit[cur], order, ld};
+        const int nxt = cur ^ 1;
+        my_min = ~0ull;
+        unsigned my_warn = 0;
+        for (int r0 = warp; r0 < ps; r0 += nwarps) {
+            const bool dr = ((cs.bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0;
+            const int slot = order[r0];
+            const UpdateResult res = update_protozoon(P, O, R, r0 + 1, dr, dr ? A.p_dr[r0] : 0.0,
+                                                      pos[nxt] + (size_t)slot * ld, ws, lane);
+            if (lane == 0) {
+                fit[nxt][slot] = res.fitness;
+                const unsigned long long k = sort_key(res.fitness);
+                keys[slot] = k;
+                my_min = k < my_min ? k : my_min;
+                my_warn += res.warned ? 1u : 0u;
+            }
+        }
+        if (lane == 0) {
+            red_min[warp] = my_min;
+            red_warn[warp] = my_warn;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long m = ~0ull;
+            for (int k = 0; k < nwarps; k++) {
+                m = red_min[k] < m ? red_min[k] : m;
+                warn_total += red_warn[k];
+            }
+            if (trace) trace[t + 1] = key_to_double(m);
+        }
+        cur = nxt;
+        __syncthreads();
+    }
+    // outputs in reference row order (row r = order[r])
+    if (threadIdx.x == 0) {
+        int best = 0;
+        for (int r = 1; r < ps; r++)
+            if (fit[cur][order[r]] < fit[cur][order[best]]) best = r;
+        red_warn[0] = (unsigned)best;
+        A.best_fit[run] = fit[cur][order[best]];
+        if (A.warnings) A.warnings[run] = warn_total;
+    }
+    __syncthreads();
+    const int bslot = order[red_warn[0]];
+    if (A.best_pos)
+        for (int d = threadIdx.x; d < dim; d += blockDim.x) A.best_pos[(size_t)run * dim + d] = pos[cur][(size_t)bslot * ld + d];
+    if (A.final_pos)
+        for (int e = threadIdx.x; e < ps * dim; e += blockDim.x) {
+            const int r = e / dim, d = e - r * dim;
+            A.final_pos[(size_t)run * ps * dim + e] = pos[cur][(size_t)order[r] * ld + d];
+        }
+    if (A.final_fit)
+        for (int r = threadIdx.x; r < ps; r += blockDim.x) A.final_fit[(size_t)run * ps + r] = fit[cur][order[r]];
+}
+
+int launch_update(bool indirect, const IterParams& P, const ObjDesc& O, const double* pos, const double* fit,
+                  const int* order, const uint8_t* in_dr_bytes, const unsigned* in_dr_bits, const double* p_dr,
+                  double* out_pos, double* out_fit, uint8_t* out_acc, uint8_t* out_warn,
+                  unsigned long long* warn_count, unsigned long long* trace_key, cudaStream_t st) {
+    const int w = warps_for_dim(P.dim);
+    const size_t smem = warp_scratch_bytes(P.dim) * (size_t)w;
+    const void* fn = indirect ? (const void*)k_update<true> : (const void*)k_update<false>;
+    if (int rc = set_smem(fn, smem)) return rc;
+    int per_sm = 1;
+    APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
+    if (per_sm < 1) per_sm = 1;
+    const long long need = ((long long)P.ps + w - 1) / w;
+    const long long cap = (long long)per_sm * num_sms();
+    const int grid = (int)(need < cap ? need : cap);
+    if (indirect)
+        k_update<true><<<grid, 32 * w, smem, st>>>(P, O, pos, fit, order, in_dr_bytes, in_dr_bits, p_dr, out_pos,
+                                                   out_fit, out_acc, out_warn, warn_count, trace_key);
+    else
+        k_update<false><<<grid, 32 * w, smem, st>>>(P, O, pos, fit, order, in_dr_bytes, in_dr_bits, p_dr, out_pos,
+                                                    out_fit, out_acc, out_warn, warn_count, trace_key);
+    APO_CUDA(cudaGetLastError());
+    return APO_OK;
+}
+
+int grid_for(long long n, int threads) {
+    long long g = (n + threads - 1) / threads;
+    long long cap = 16LL * num_sms();
+    if (g < 1) g = 1;
+    return (int)(g < cap ? g : cap);
+}
+
+int nbits_for(long long n) {
+    int b = 1;
+    while ((1LL << b) < n) b++;
+    return b;
+}
+
+uint64_t coord_count(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_max) {
+    const uint64_t cbase = stream_base(seed, key_iteration, kCoordinator);
+    const double pf = pf_max * uniform(cbase, 0);
+    return (uint64_t)ceil((double)ps * pf);
+}
+
+// Coordinator Dr on device given scratch (keys + sorted keys + CUB temp).
+int dr_device(uint64_t seed, uint64_t key_iteration, int64_t ps, int64_t count, unsigned long long* keys,
+              unsigned long long* keys_sorted, void* tmp, size_t tmp_bytes, unsigned* bits, uint8_t* bytes,
+              cudaStream_t st) {
+    if (bits) APO_CUDA(cudaMemsetAsync(bits, 0, 4 * (size_t)((ps + 31) / 32), st));
+    if (bytes) APO_CUDA(cudaMemsetAsync(bytes, 0, (size_t)ps, st));
+    if (count <= 0) return APO_OK;
+    const uint64_t cbase = stream_base(seed, key_iteration, kCoordinator);
+    k_dr_draw<<<grid_for(count, 256), 256, 0, st>>>((int)count, (int)ps, cbase, keys);
+    APO_CUDA(cudaGetLastError());
+    size_t bytes_needed = tmp_bytes;
+    APO_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes_needed, keys, keys_sorted, (int)count, 0,
+                                            32 + nbits_for(ps), st));
+    k_dr_resolve<<<grid_for(count, 256), 256, 0, st>>>((int)count, (int)ps, cbase, keys_sorted, bits, bytes);
+    APO_CUDA(cudaGetLastError());
+    return APO_OK;
+}
+
+size_t dr_tmp_bytes(int64_t cap, int64_t ps) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, b, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                   (int)(cap > 0 ? cap : 1), 0, 32 + nbits_for(ps));
+    return b;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+struct apo_run {
+    int64_t ps, dim, ld, T;
+    uint64_t seed;
+    int64_t npairs;
+    double pf_max, lower, upper, eps;
+    ObjDesc obj;
+    cudaStream_t stream;
+    double* pos[2];
+    double* fit[2];
+    int cur;
+    int* order;
+    unsigned long long* keys_in;
+    unsigned long long* keys_out;
+    int* vals_in;
+    unsigned long long* dr_keys;
+    unsigned long long* dr_sorted;
+    unsigned* dr_bits;
+    int64_t dr_cap;
+    void* tmp;
+    size_t tmp_bytes;
+    double* p_dr;
+    std::vector<double> sched;
+    unsigned long long* trace_keys;  // [T+1]
+    unsigned long long* warn;
+    int64_t iters;
+    bool initialized;
+};
+
+extern "C" {
+
+int apo_abi_version(void) { return 1; }
+
+const char* apo_last_error(void) { return g_err.c_str(); }
+
+int apo_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int apo_run_updates_obj(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
+                        double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim, uint64_t seed,
+                        uint64_t key_iteration, int64_t npairs, double lower, double upper, double eps, double p_ah,
+                        double f_mult, double decay, const apo_objective* objective_host, const double* p_dr,
+                        unsigned long long* warn_count, void* stream) {
+    APO_CHECK(ps >= 1 && ps < (1LL << 31), "ps out of range");
+    APO_CHECK(dim >= 1 && dim <= 8192, "dim out of range (1..8192)");
+    APO_CHECK(npairs >= 1, "npairs must be >= 1");
+    APO_CHECK(positions && fitness && in_dr && out_pos && out_fit && p_dr, "NULL buffer");
+    APO_CHECK(out_pos != positions && out_fit != fitness, "outputs must not alias inputs");
+    if (int rc = check_objective(objective_host, dim)) return rc;
+    IterParams P;
+    P.seed = seed;
+    P.key_iteration = key_iteration;
+    P.ps = (int)ps;
+    P.dim = (int)dim;
+    P.npairs = (int)npairs;
+    P.ld = (int)dim;
+    P.lower = lower;
+    P.upper = upper;
+    P.span = upper - lower;
+    P.eps = eps;
+    P.p_ah = p_ah;
+    P.f_mult = f_mult;
+    P.decay = decay;
+    if (warn_count) APO_CUDA(cudaMemsetAsync(warn_count, 0, sizeof(unsigned long long), as_stream(stream)));
+    return launch_update(false, P, to_desc(objective_host), positions, fitness, nullptr, in_dr, nullptr, p_dr,
+                         out_pos, out_fit, out_acc, out_warn, warn_count, nullptr, as_stream(stream));
+}
+
+int apo_run_updates(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
+                    double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim, uint64_t seed,
+                    uint64_t key_iteration, int64_t npairs, double lower, double upper, double span, double eps,
+                    double p_ah, double f_mult, double decay, int64_t code, const double* table, int64_t table_len,
+                    const double* p_dr, unsigned long long* warn_count, void* stream) {
+    APO_CHECK(span == upper - lower, "span must equal upper - lower");
+    apo_objective o;
+    o.code = (int32_t)code;
+    o.table_len = (int32_t)table_len;
+    o.table = table;
+    return apo_run_updates_obj(positions, fitness, in_dr, out_pos, out_fit, out_acc, out_warn, ps, dim, seed,
+                               key_iteration, npairs, lower, upper, eps, p_ah, f_mult, decay, &o, p_dr, warn_count,
+                               stream);
+}
+
+int apo_evaluate(const double* x, int64_t n, int64_t dim, int64_t ld, const apo_objective* objective_host, double* out,
+                 void* stream) {
+    APO_CHECK(n >= 0 && dim >= 1 && dim <= 8192 && ld >= dim, "bad shape");
+    if (int rc = check_objective(objective_host, dim)) return rc;
+    if (n == 0) return APO_OK;
+    const int w = warps_for_dim(dim);
+    const size_t smem = warp_scratch_bytes((int)dim) * (size_t)w;
+    if (int rc = set_smem((const void*)k_evaluate, smem)) return rc;
+    const long long need = (n + w - 1) / w;
+    const long long cap = 8LL * num_sms();
+    k_evaluate<<<(int)(need < cap ? need : cap), 32 * w, smem, as_stream(stream)>>>(x, (int)n, (int)dim, (int)ld,
+                                                                                  to_desc(objective_host), out);
+    APO_CUDA(cudaGetLastError());
+    return APO_OK;
+}
+
+int apo_initialize(uint64_t seed, int64_t ps, int64_t dim, int64_t ld, double lower, double span,
+                   const apo_objective* objective_host, double* positions, double* fitness, void* stream) {
+    APO_CHECK(ps >= 1 && ps < (1LL << 31) && dim >= 1 && dim <= 8192 && ld >= dim, "bad shape");
+    APO_CHECK(positions && fitness, "NULL buffer");
+    if (int rc = check_objective(objective_host, dim)) return rc;
+    const int w = warps_for_dim(dim);
+    const size_t smem = warp_scratch_bytes((int)dim) * (size_t)w;
+    if (int rc = set_smem((const void*)k_init, smem)) return rc;
+    const long long need = (ps + w - 1) / w;
+    const long long cap = 8LL * num_sms();
+    k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, as_stream(stream)>>>(
+        seed, (int)ps, (int)dim, (int)ld, lower, span, to_desc(objective_host), positions, fitness, nullptr);
+    APO_CUDA(cudaGetLastError());
+    return APO_OK;
+}
+
+int apo_sort_order(const double* fitness, int64_t n, int32_t* order, void* stream) {
+    APO_CHECK(n >= 0 && n < (1LL << 31), "n out of range");
+    if (n == 0) return APO_OK;
+    cudaStream_t st = as_stream(stream);
+    unsigned long long *k_in = nullptr, *k_out = nullptr;
+    int* v_in = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    APO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, v_in, (int*)order, (int)n, 0, 64, st));
+    APO_CUDA(cudaMallocAsync((void**)&k_in, 8 * (size_t)n, st));
+    APO_CUDA(cudaMallocAsync((void**)&k_out, 8 * (size_t)n, st));
+    APO_CUDA(cudaMallocAsync((void**)&v_in, 4 * (size_t)n, st));
+    APO_CUDA(cudaMallocAsync(&tmp, tb, st));
+    k_make_keys<<<grid_for(n, 256), 256, 0, st>>>((int)n, fitness, nullptr, k_in, v_in);
+    APO_CUDA(cudaGetLastError());
+    APO_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, v_in, (int*)order, (int)n, 0, 64, st));
+    cudaFreeAsync(k_in, st);
+    cudaFreeAsync(k_out, st);
+    cudaFreeAsync(v_in, st);
+    cudaFreeAsync(tmp, st);
+    return APO_OK;
+}
+
+int apo_select_dr(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_max, uint8_t* in_dr,
+                  int64_t* count_host, void* stream) {
+    APO_CHECK(ps >= 1 && ps < (1LL << 31) && in_dr, "bad arguments");
+    APO_CHECK(pf_max > 0.0 && pf_max <= 1.0, "pf_max must be in (0, 1]");
+    cudaStream_t st = as_stream(stream);
+    const int64_t count = (int64_t)coord_count(seed, key_iteration, ps, pf_max);
+    if (count_host) *count_host = count;
+    unsigned long long *keys = nullptr, *sorted = nullptr;
+    void* tmp = nullptr;
+    size_t tb = dr_tmp_bytes(count, ps);
+    if (count > 0) {
+        APO_CUDA(cudaMallocAsync((void**)&keys, 8 * (size_t)count, st));
+        APO_CUDA(cudaMallocAsync((void**)&sorted, 8 * (size_t)count, st));
+        APO_CUDA(cudaMallocAsync(&tmp, tb, st));
+    }
+    int rc = dr_device(seed, key_iteration, ps, count, keys, sorted, tmp, tb, nullptr, in_dr, st);
+    if (count > 0) {
+        cudaFreeAsync(keys, st);
+        cudaFreeAsync(sorted, st);
+        cudaFreeAsync(tmp, st);
+    }
+    return rc;
+}
+
+int apo_histogram_u8(const uint8_t* pixels, int64_t n, int64_t* counts, void* stream) {
+    APO_CHECK(n >= 0 && counts && (n == 0 || pixels), "bad arguments");
+    APO_CHECK(((uintptr_t)pixels & 15) == 0, "pixels must be 16-byte aligned");
+    cudaStream_t st = as_stream(stream);
+    APO_CUDA(cudaMemsetAsync(counts, 0, 256 * sizeof(int64_t), st));
+    if (n == 0) return APO_OK;
+    long long g = (n / 16 + kThreads - 1) / kThreads;
+    const long long cap = 4LL * num_sms();
+    if (g < 1) g = 1;
+    k_histogram_u8<<<(int)(g < cap ? g : cap), kThreads, 0, st>>>(pixels, n, (unsigned long long*)counts);
+    APO_CUDA(cudaGetLastError());
+    return APO_OK;
+}
+
+int apo_debug_exp(const double* x, double* out, int64_t n, void* stream) {
+    APO_CHECK(n >= 0, "bad n");
+    if (n == 0) return APO_OK;
+    k_debug_exp<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(x, out, n);
+    APO_CUDA(cudaGetLastError());
+    return APO_OK;
+}
+
+// --------------------------- device-resident run ---------------------------
+
+int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iterations, uint64_t seed, int64_t npairs,
+                   double pf_max, double lower, double upper, double eps, const apo_objective* objective_host,
+                   const double* sched_host, const double* p_dr_host, void* stream) {
+    APO_CHECK(out != nullptr, "out is NULL");
+    APO_CHECK(ps >= 1 && ps < (1LL << 31) && dim >= 1 && dim <= 8192, "bad shape");
+    APO_CHECK(max_iterations >= 0 && npairs >= 1 && pf_max > 0.0 && pf_max <= 1.0, "bad config");
+    APO_CHECK(max_iterations == 0 || sched_host, "sched_host is NULL");
+    APO_CHECK(p_dr_host, "p_dr_host is NULL");
+    if (int rc = check_objective(objective_host, dim)) return rc;
+    apo_run* r = new apo_run();
+    r->ps = ps;
+    r->dim = dim;
+    r->ld = (dim + 1) & ~1LL;  // 16-byte aligned rows
+    r->T = max_iterations;
+    r->seed = seed;
+    r->npairs = npairs;
+    r->pf_max = pf_max;
+    r->lower = lower;
+    r->upper = upper;
+    r->eps = eps;
+    r->obj = to_desc(objective_host);
+    r->stream = as_stream(stream);
+    r->cur = 0;
+    r->iters = 0;
+    r->initialized = false;
+    r->sched.assign(sched_host, sched_host + 3 * max_iterations);
+    r->dr_cap = (int64_t)ceil((double)ps * pf_max) + 1;
+    const size_t rows = 8 * (size_t)ps * (size_t)r->ld;
+    cudaStream_t st = r->stream;
+    size_t tb_sort = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (int*)nullptr, (int*)nullptr, (int)ps, 0, 64, st);
+    const size_t tb_dr = dr_tmp_bytes(r->dr_cap, ps);
+    r->tmp_bytes = tb_sort > tb_dr ? tb_sort : tb_dr;
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](void** p, size_t b) {
+        if (e == cudaSuccess) e = cudaMalloc(p, b > 0 ? b : 16);
+    };
+    alloc((void**)&r->pos[0], rows);
+    alloc((void**)&r->pos[1], rows);
+    alloc((void**)&r->fit[0], 8 * (size_t)ps);
+    alloc((void**)&r->fit[1], 8 * (size_t)ps);
+    alloc((void**)&r->order, 4 * (size_t)ps);
+    alloc((void**)&r->keys_in, 8 * (size_t)ps);
+    alloc((void**)&r->keys_out, 8 * (size_t)ps);
+    alloc((void**)&r->vals_in, 4 * (size_t)ps);
+    alloc((void**)&r->dr_keys, 8 * (size_t)r->dr_cap);
+    alloc((void**)&r->dr_sorted, 8 * (size_t)r->dr_cap);
+    alloc((void**)&r->dr_bits, 4 * (size_t)((ps + 31) / 32));
+    alloc(&r->tmp, r->tmp_bytes);
+    alloc((void**)&r->p_dr, 8 * (size_t)ps);
+    alloc((void**)&r->trace_keys, 8 * (size_t)(max_iterations + 1));
+    alloc((void**)&r->warn, 8);
+    if (e != cudaSuccess) {
+        apo_run_destroy(r);
+        return fail(APO_ENOMEM, std::string("apo_run_create: ") + cudaGetErrorString(e));
+    }
+    APO_CUDA(cudaMemcpyAsync(r->p_dr, p_dr_host, 8 * (size_t)ps, cudaMemcpyHostToDevice, st));
+    APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(max_iterations + 1), st));
+    APO_CUDA(cudaMemsetAsync(r->warn, 0, 8, st));
+    *out = r;
+    return APO_OK;
+}
+
+int apo_run_initialize(apo_run* r) {
+    APO_CHECK(r, "run is NULL");
+    cudaStream_t st = r->stream;
+    const int w = warps_for_dim(r->dim);
+    const size_t smem = warp_scratch_bytes((int)r->dim) * (size_t)w;
+    if (int rc = set_smem((const void*)k_init, smem)) return rc;
+    int per_sm = 1;
+    APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_init, 32 * w, smem));
+    const long long need = (r->ps + w - 1) / w;
+    const long long cap = (long long)(per_sm > 0 ? per_sm : 1) * num_sms();
+    APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(r->T + 1), st));
+    APO_CUDA(cudaMemsetAsync(r->warn, 0, 8, st));
+    k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, st>>>(r->seed, (int)r->ps, (int)r->dim, (int)r->ld,
+                                                                  r->lower, r->upper - r->lower, r->obj, r->pos[0],
+                                                                  r->fit[0], r->trace_keys);
+    APO_CUDA(cudaGetLastError());
+    k_iota<<<grid_for(r->ps, 256), 256, 0, st>>>((int)r->ps, r->order);
+    APO_CUDA(cudaGetLastError());
+    r->cur = 0;
+    r->iters = 0;
+    r->initialized = true;
+    return APO_OK;
+}
+
+int apo_run_iterate(apo_run* r, int64_t n) {
+    APO_CHECK(r && r->initialized, "run not initialised");
+    APO_CHECK(n >= 0 && r->iters + n <= r->T, "iteration budget exceeded");
+    cudaStream_t st = r->stream;
+    const int ps = (int)r->ps;
+    for (int64_t k = 0; k < n; k++) {
+        const int64_t t = r->iters;
+        const uint64_t key_it = (uint64_t)t + 1;
+        // 1. stable sort by fitness, ties by previous rank
+        k_make_keys<<<grid_for(ps, 256), 256, 0, st>>>(ps, r->fit[r->cur], r->order, r->keys_in, r->vals_in);
+        APO_CUDA(cudaGetLastError());
+        size_t tb = r->tmp_bytes;
+        APO_CUDA(cub::DeviceRadixSort::SortPairs(r->tmp, tb, r->keys_in, r->keys_out, r->vals_in, r->order, ps, 0, 64,
+                                                 st));
+        // 2. coordinator draws
+        const int64_t count = (int64_t)coord_count(r->seed, key_it, r->ps, r->pf_max);
+        if (int rc = dr_device(r->seed, key_it, r->ps, count, r->dr_keys, r->dr_sorted, r->tmp, r->tmp_bytes,
+                               r->dr_bits, nullptr, st))
+            return rc;
+        // 3. fused update
+        IterParams P;
+        P.seed = r->seed;
+        P.key_iteration = key_it;
+        P.ps = ps;
+        P.dim = (int)r->dim;
+        P.npairs = (int)r->npairs;
+        P.ld = (int)r->ld;
+        P.lower = r->lower;
+        P.upper = r->upper;
+        P.span = r->upper - r->lower;
+        P.eps = r->eps;
+        P.p_ah = r->sched[3 * t];
+        P.f_mult = r->sched[3 * t + 1];
+        P.decay = r->sched[3 * t + 2];
+        if (int rc = launch_update(true, P, r->obj, r->pos[r->cur], r->fit[r->cur], r->order, nullptr, r->dr_bits,
+                                   r->p_dr, r->pos[r->cur ^ 1], r->fit[r->cur ^ 1], nullptr, nullptr, r->warn,
+                                   r->trace_keys + t + 1, st))
+            return rc;
+        r->cur ^= 1;
+        r->iters++;
+    }
+    return APO_OK;
+}
+
+int apo_run_trace(apo_run* r, double* trace_host, int64_t n) {
+    APO_CHECK(r && trace_host && n >= 0 && n <= r->T, "bad arguments");
+    std::vector<unsigned long long> k((size_t)n + 1);
+    APO_CUDA(cudaMemcpyAsync(k.data(), r->trace_keys, 8 * ((size_t)n + 1), cudaMemcpyDeviceToHost, r->stream));
+    APO_CUDA(cudaStreamSynchronize(r->stream));
+    for (int64_t a = 0; a <= n; a++) trace_host[a] = key_to_double(k[(size_t)a]);
+    return APO_OK;
+}
+
+int apo_run_population(apo_run* r, double* positions, double* fitness, int is_host) {
+    APO_CHECK(r && r->initialized, "run not initialised");
+    cudaStream_t st = r->stream;
+    double* dpos = positions;
+    double* dfit = fitness;
+    if (is_host) {
+        APO_CUDA(cudaMallocAsync((void**)&dpos, 8 * (size_t)r->ps * r->dim, st));
+        APO_CUDA(cudaMallocAsync((void**)&dfit, 8 * (size_t)r->ps, st));
+    }
+    k_gather_rows<<<grid_for(r->ps * 32, 256), 256, 0, st>>>((int)r->ps, (int)r->dim, (int)r->ld, r->pos[r->cur],
+                                                             r->fit[r->cur], r->order, dpos, dfit);
+    APO_CUDA(cudaGetLastError());
+    if (is_host) {
+        if (positions)
+            APO_CUDA(cudaMemcpyAsync(positions, dpos, 8 * (size_t)r->ps * r->dim, cudaMemcpyDeviceToHost, st));
+        if (fitness) APO_CUDA(cudaMemcpyAsync(fitness, dfit, 8 * (size_t)r->ps, cudaMemcpyDeviceToHost, st));
+        cudaFreeAsync(dpos, st);
+        cudaFreeAsync(dfit, st);
+        APO_CUDA(cudaStreamSynchronize(st));
+    }
+    return APO_OK;
+}
+
+int apo_run_best(apo_run* r, double* best_fitness_host, double* best_position_host, int64_t* best_row_host) {
+    APO_CHECK(r && r->initialized, "run not initialised");
+    std::vector<double> fit((size_t)r->ps);
+    std::vector<int> order((size_t)r->ps);
+    cudaStream_t st = r->stream;
+    APO_CUDA(cudaMemcpyAsync(order.data(), r->order, 4 * (size_t)r->ps, cudaMemcpyDeviceToHost, st));
+    APO_CUDA(cudaMemcpyAsync(fit.data(), r->fit[r->cur], 8 * (size_t)r->ps, cudaMemcpyDeviceToHost, st));
+    APO_CUDA(cudaStreamSynchronize(st));
+    int64_t best = 0;
+    for (int64_t a = 1; a < r->ps; a++)
+        if (fit[(size_t)order[(size_t)a]] < fit[(size_t)order[(size_t)best]]) best = a;
+    const int slot = order[(size_t)best];
+    if (best_fitness_host) *best_fitness_host = fit[(size_t)slot];
+    if (best_row_host) *best_row_host = best;
+    if (best_position_host) {
+        APO_CUDA(cudaMemcpyAsync(best_position_host, r->pos[r->cur] + (size_t)slot * r->ld, 8 * (size_t)r->dim,
+                                 cudaMemcpyDeviceToHost, st));
+        APO_CUDA(cudaStreamSynchronize(st));
+    }
+    return APO_OK;
+}
+
+int apo_run_counters(apo_run* r, int64_t* iterations_run, int64_t* fe_count, int64_t* warnings) {
+    APO_CHECK(r, "run is NULL");
+    unsigned long long w = 0;
+    APO_CUDA(cudaMemcpyAsync(&w, r->warn, 8, cudaMemcpyDeviceToHost, r->stream));
+    APO_CUDA(cudaStreamSynchronize(r->stream));
+    if (iterations_run) *iterations_run = r->iters;
+    if (fe_count) *fe_count = r->ps * (1 + r->iters);
+    if (warnings) *warnings = (int64_t)w;
+    return APO_OK;
+}
+
+int apo_run_destroy(apo_run* r) {
+    if (!r) return APO_OK;
+    void* bufs[] = {r->pos[0], r->pos[1], r->fit[0], r->fit[1], r->order, r->keys_in, r->keys_out, r->vals_in,
+                    r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    delete r;
+    return APO_OK;
+}
+
+// ------------------------------ batched runs -------------------------------
+
+int64_t apo_run_batch_max_elems(int64_t ps, int64_t dim) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
+    const int64_t ld = (dim + 1) & ~1LL;
+    const BatchLayout L = batch_layout((int)ps, (int)dim, (int)ld, kWarps);
+    return (int64_t)L.total + 2048 <= optin ? ps * dim : 0;
+}
+
+int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* objectives_host, int64_t ps,
+                  int64_t dim, int64_t max_iterations, int64_t n_iters, int64_t npairs, double pf_max, double lower,
+                  double upper, double eps, const double* sched, const double* p_dr, double* best_fit,
+                  double* best_pos, double* trace, double* final_pos, double* final_fit, int64_t* warnings,
+                  void* stream) {
+    APO_CHECK(nruns >= 1 && nruns < (1LL << 31), "nruns out of range");
+    APO_CHECK(ps >= 1 && dim >= 1 && dim <= 8192, "bad shape");
+    APO_CHECK(n_iters >= 0 && n_iters <= max_iterations, "n_iters must be in [0, max_iterations]");
+    APO_CHECK(npairs >= 1 && pf_max > 0.0 && pf_max <= 1.0, "bad config");
+    APO_CHECK(seeds && objectives_host && best_fit && p_dr && (n_iters == 0 || sched), "NULL buffer");
+    for (int64_t k = 0; k < nruns; k++)
+        if (int rc = check_objective(&objectives_host[k], dim)) return rc;
+    APO_CHECK(apo_run_batch_max_elems(ps, dim) > 0, "population too large for the shared-memory batch kernel");
+    cudaStream_t st = as_stream(stream);
+    std::vector<ObjDesc> descs((size_t)nruns);
+    for (int64_t k = 0; k < nruns; k++) descs[(size_t)k] = to_desc(&objectives_host[k]);
+    ObjDesc* d_descs = nullptr;
+    APO_CUDA(cudaMallocAsync((void**)&d_descs, sizeof(ObjDesc) * (size_t)nruns, st));
+    APO_CUDA(cudaMemcpyAsync(d_descs, descs.data(), sizeof(ObjDesc) * (size_t)nruns, cudaMemcpyHostToDevice, st));
+    BatchArgs A;
+    A.seeds = seeds;
+    A.objs = d_descs;
+    A.ps = (int)ps;
+    A.dim = (int)dim;
+    A.ld = (int)((dim + 1) & ~1LL);
+    A.max_iterations = (int)max_iterations;
+    A.n_iters = (int)n_iters;
+    A.npairs = (int)npairs;
+    A.pf_max = pf_max;
+    A.lower = lower;
+    A.upper = upper;
+    A.span = upper - lower;
+    A.eps = eps;
+    A.sched = sched;
+    A.p_dr = p_dr;
+    A.best_fit = best_fit;
+    A.best_pos = best_pos;
+    A.trace = trace;
+    A.final_pos = final_pos;
+    A.final_fit = final_fit;
+    A.warnings = (long long*)warnings;
+    const BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps);
+    if (int rc = set_smem((const void*)k_run_batch, L.total)) return rc;
+    k_run_batch<<<(int)nruns, kThreads, L.total, st>>>(A);
+    APO_CUDA(cudaGetLastError());
+    cudaFreeAsync(d_descs, st);
+    return APO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// apo_objective.cuh -- fitness evaluation, one candidate per warp.
+//
+// Basic functions: numba_backend.py:93-138 (== objectives.py:105-152).  The
+// reference accumulates strictly left to right; in oracle mode lanes compute
+// the per-dimension terms in parallel (each term is rounded exactly as in
+// the reference) and lane 0 then accumulates them in order, so the sum is
+// bit-identical.  Table lookup: objectives.py:213-219.
+#pragma once
+#include "apo_device.cuh"
+
+namespace apo {
+
+enum ObjCode : int {
+    OBJ_SPHERE = 0,
+    OBJ_BENT_CIGAR = 1,
+    OBJ_ELLIPTIC = 2,
+    OBJ_HGBAT = 3,
+    OBJ_ROSENBROCK = 4,
+    OBJ_GRIEWANK = 5,
+    OBJ_TABLE = 6,
+};
+
+// Objective descriptor; all pointers are device pointers.
+struct ObjDesc {
+    int code;
+    int table_len;
+    const double* table;  // elliptic weights (code 2) or value table (code 6)
+};
+
+__device__ __forceinline__ double warp_bcast(double v, int src) { return __shfl_sync(0xFFFFFFFFu, v, src); }
+
+// c: candidate [dim] (shared), t: scratch [dim] (shared).  Returns the
+// fitness on every lane.
+__device__ inline double eval_warp(const ObjDesc& O, const double* c, double* t, int dim, int lane) {
+    double f = 0.0;
+    switch (O.code) {
+    case OBJ_SPHERE:
+        for (int d = lane; d < dim; d += 32) t[d] = c[d] * c[d];
+        __syncwarp();
+        if (lane == 0) {
+            double s = 0.0;
+            for (int d = 0; d < dim; d++) s += t[d];
+            f = s;
+        }
+        break;
+    case OBJ_BENT_CIGAR:
+        for (int d = lane; d < dim; d += 32) t[d] = c[d] * c[d];
+        __syncwarp();
+        if (lane == 0) {
+            double s = 0.0;
+            for (int d = 1; d < dim; d++) s += t[d];
+            f = t[0] + 1e6 * s;
+        }
+        break;
+    case OBJ_ELLIPTIC:
+        for (int d = lane; d < dim; d += 32) t[d] = (O.table[d] * c[d]) * c[d];
+        __syncwarp();
+        if (lane == 0) {
+            double s = 0.0;
+            for (int d = 0; d < dim; d++) s += t[d];
+            f = s;
+        }
+        break;
+    case OBJ_HGBAT:
+        for (int d = lane; d < dim; d += 32) t[d] = c[d] * c[d];
+        __syncwarp();
+        if (lane == 0) {
+            double s1 = 0.0, s2 = 0.0;
+            for (int d = 0; d < dim; d++) {
+                s1 += c[d];
+                s2 += t[d];
+            }
+            f = sqrt(fabs(s2 * s2 - s1 * s1)) + (0.5 * s2 + s1) / (double)dim + 0.5;
+        }
+        break;
+    case OBJ_ROSENBROCK:
+        for (int d = lane; d < dim - 1; d += 32) {
+            const double a = c[d + 1] - c[d] * c[d];
+            const double b = c[d] - 1.0;
+            t[d] = 100.0 * (a * a) + b * b;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double s = 0.0;
+            for (int d = 0; d < dim - 1; d++) s += t[d];
+            f = s;
+        }
+        break;
+    case OBJ_GRIEWANK:
+        // cos through CUDA's libdevice (<= 1-2 ulp); glibc's cos is not
+        // ported, so griewank agrees to ~1e-15 relative, not bit for bit.
+        for (int d = lane; d < dim; d += 32) t[d] = cos(c[d] / sqrt((double)d + 1.0));
+        __syncwarp();
+        if (lane == 0) {
+            double s = 0.0, p = 1.0;
+            for (int d = 0; d < dim; d++) {
+                s += c[d] * c[d];
+                p *= t[d];
+            }
+            f = 1.0 + s / 4000.0 - p;
+        }
+        break;
+    default: {  // OBJ_TABLE: table[round_half_up(x0)], clamped
+        if (lane == 0) {
+            long long idx = (long long)floor(c[0] + 0.5);
+            if (idx < 0) idx = 0;
+            if (idx > O.table_len - 1) idx = O.table_len - 1;
+            f = O.table[idx];
+        }
+        break;
+    }
+    }
+    f = warp_bcast(f, 0);
+    __syncwarp();
+    return f;
+}
+
+}  // namespace apo

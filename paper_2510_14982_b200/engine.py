@@ -1,0 +1,431 @@
+"""Run orchestration on the B200 (API parity with protozoa.engine).
+
+``initialize`` / ``step`` / ``run`` / ``benchmark`` keep the reference's
+signatures and results (engine.py:116-284).  What changes is where the loop
+lives:
+
+* ``step`` performs the reference's three phases on the device -- stable
+  sort (C-ABI ``apo_sort_order``), coordinator draws (``apo_select_dr``) and
+  the fused update (``run_updates`` of the cuda backend);
+* ``run`` never returns to the host per iteration: small populations run in
+  one persistent CTA with the population in shared memory
+  (``apo_run_batch``), large ones in the device-resident loop
+  (``apo_run_*``: key sort -> Dr -> one fused update launch per iteration);
+* ``run_many`` batches independent (seed, objective) runs, one CTA each, and
+  shards them across GPUs when torch.distributed is initialised (no
+  collective; results gathered once at the end).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field, replace
+from statistics import fmean
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib, kernels
+from .core import ApoConfig, ConfigError, Population, p_dr_table, schedule_table
+from .objectives import EXTERNAL, Objective, device_objective, resolve_objective
+
+SEQUENTIAL = "sequential"
+PARALLEL = "parallel"
+
+# Largest population routed to the single-CTA shared-memory kernel by run().
+BATCH_PS_LIMIT = 256
+
+
+@dataclass(frozen=True)
+class EngineMode:
+    """``sequential`` or ``parallel`` (engine.py:40-65).  On the device both
+    modes run the same kernels; results never depend on the mode."""
+
+    kind: str = SEQUENTIAL
+    workers: object = None
+
+    def __post_init__(self) -> None:
+        if self.kind not in (SEQUENTIAL, PARALLEL):
+            raise ValueError(f"kind must be {SEQUENTIAL!r} or {PARALLEL!r}, got {self.kind!r}")
+        w = self.workers
+        if w is not None and w != "auto" and not (isinstance(w, int) and w >= 1):
+            raise ValueError(f"workers must be a positive integer or 'auto', got {w!r}")
+
+    @staticmethod
+    def sequential() -> "EngineMode":
+        return EngineMode(SEQUENTIAL)
+
+    @staticmethod
+    def parallel(workers: object = "auto") -> "EngineMode":
+        return EngineMode(PARALLEL, workers)
+
+
+@dataclass
+class RunResult:
+    """Outcome of one run (engine.py:68-89)."""
+
+    best_position: np.ndarray
+    best_fitness: float
+    trace: np.ndarray
+    iterations_run: int
+    fe_count: int
+    warnings: int
+    wall_clock_seconds: float
+    mode: str
+    workers: int
+    backend: str
+    config_echo: ApoConfig
+    population: Population = field(repr=False, default=None)
+
+
+def _resolve_backend(objective: Objective, backend: Optional[str]):
+    if objective.code == EXTERNAL:
+        raise ValueError("external objective functions need the reference's numpy backend; "
+                         "the cuda backend evaluates objectives on the device")
+    return kernels.get_backend(backend)
+
+
+def resolve_workers(mode: EngineMode, backend) -> int:
+    if mode.kind == SEQUENTIAL:
+        return 1
+    cap = max(1, int(backend.max_workers()))
+    if mode.workers in (None, "auto"):
+        return cap
+    return min(int(mode.workers), cap)
+
+
+def _check(cfg: ApoConfig, obj: Objective) -> None:
+    bad = cfg.violations()
+    if bad:
+        raise ConfigError("invalid configuration:\n" + "\n".join(f"  - {b}" for b in bad))
+    if cfg.dim < obj.min_dim:
+        raise ConfigError(f"objective {obj.name!r} needs dim >= {obj.min_dim}, got dim = {cfg.dim}")
+
+
+def _dev():
+    import torch
+
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def initialize(cfg: ApoConfig, objective) -> Population:
+    """Iteration-0 population on the device (engine.py:116-139); fe_count = ps."""
+    import torch
+
+    obj = resolve_objective(objective)
+    _check(cfg, obj)
+    if obj.code == EXTERNAL:
+        raise ValueError("external objective functions cannot run on the cuda backend")
+    lib = _lib.require_cuda()
+    pos = torch.empty((cfg.ps, cfg.dim), dtype=torch.float64, device=_dev())
+    fit = torch.empty(cfg.ps, dtype=torch.float64, device=pos.device)
+    dobj = device_objective(obj, cfg.dim)
+    _lib.check(lib.apo_initialize(cfg.seed, cfg.ps, cfg.dim, cfg.dim, cfg.bounds.lower, cfg.bounds.span, dobj.ref,
+                                  _lib.ptr(pos), _lib.ptr(fit), _lib.stream_handle()), "apo_initialize")
+    return Population(pos.cpu().numpy(), fit.cpu().numpy(), iteration=0, fe_count=cfg.ps, warnings=0)
+
+
+def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: EngineMode = None,
+         backend: Optional[str] = None) -> Population:
+    """One full iteration; returns the next population, input untouched (engine.py:142-172)."""
+    import torch
+
+    mode = mode or EngineMode.sequential()
+    obj = resolve_objective(objective)
+    if pop.size != cfg.ps or pop.dim != cfg.dim:
+        raise ValueError(f"population shape ({pop.size}, {pop.dim}) does not match config "
+                         f"(ps={cfg.ps}, dim={cfg.dim})")
+    bk = _resolve_backend(obj, backend)
+    workers = resolve_workers(mode, bk)
+    lib = _lib.require_cuda()
+    dev = _dev()
+    stream = _lib.stream_handle()
+    pos = torch.as_tensor(pop.positions, device=dev)
+    fit = torch.as_tensor(pop.fitness, device=dev)
+    order = torch.empty(cfg.ps, dtype=torch.int32, device=dev)
+    _lib.check(lib.apo_sort_order(_lib.ptr(fit), cfg.ps, _lib.ptr(order), stream), "apo_sort_order")
+    order = order.long()
+    snap_pos = pos.index_select(0, order).contiguous()
+    snap_fit = fit.index_select(0, order).contiguous()
+    in_dr = torch.empty(cfg.ps, dtype=torch.uint8, device=dev)
+    _lib.check(lib.apo_select_dr(cfg.seed, iteration + 1, cfg.ps, cfg.pf_max, _lib.ptr(in_dr), None, stream),
+               "apo_select_dr")
+    new_pos, new_fit, _acc, warned = bk.run_updates(snap_pos, snap_fit, in_dr, cfg, obj, iteration, iteration + 1,
+                                                    parallel=(mode.kind == PARALLEL), workers=workers)
+    return Population(new_pos.cpu().numpy(), new_fit.cpu().numpy(), iteration=iteration + 1,
+                      fe_count=pop.fe_count + cfg.ps, warnings=pop.warnings + warned)
+
+
+# ---------------------------------------------------------------------------
+# device-resident runs
+
+
+class DeviceRun:
+    """A population resident in HBM driven by the C-ABI run handle."""
+
+    def __init__(self, cfg: ApoConfig, obj: Objective, stream=None):
+        import torch
+
+        self.lib = _lib.require_cuda()
+        self.cfg = cfg
+        self.obj = obj
+        self.dobj = device_objective(obj, cfg.dim)
+        self.stream = stream
+        sched = np.ascontiguousarray(schedule_table(cfg.max_iterations)) if cfg.max_iterations else np.zeros(3)
+        pdr = np.ascontiguousarray(p_dr_table(cfg.ps))
+        h = C.c_void_p()
+        _lib.check(self.lib.apo_run_create(C.byref(h), cfg.ps, cfg.dim, cfg.max_iterations, cfg.seed,
+                                           cfg.neighbor_pairs, cfg.pf_max, cfg.bounds.lower, cfg.bounds.upper,
+                                           cfg.eps, self.dobj.ref, sched.ctypes.data, pdr.ctypes.data,
+                                           _lib.stream_handle(stream)), "apo_run_create")
+        self.handle = h
+        self._torch = torch
+
+    def initialize(self):
+        _lib.check(self.lib.apo_run_initialize(self.handle), "apo_run_initialize")
+
+    def iterate(self, n: int):
+        _lib.check(self.lib.apo_run_iterate(self.handle, n), "apo_run_iterate")
+
+    def counters(self):
+        it, fe, w = C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.check(self.lib.apo_run_counters(self.handle, C.byref(it), C.byref(fe), C.byref(w)), "apo_run_counters")
+        return it.value, fe.value, w.value
+
+    def trace(self, n: int) -> np.ndarray:
+        out = np.empty(n + 1)
+        _lib.check(self.lib.apo_run_trace(self.handle, out.ctypes.data, n), "apo_run_trace")
+        return out
+
+    def best(self):
+        f = C.c_double()
+        row = C.c_int64()
+        x = np.empty(self.cfg.dim)
+        _lib.check(self.lib.apo_run_best(self.handle, C.byref(f), x.ctypes.data, C.byref(row)), "apo_run_best")
+        return f.value, x, row.value
+
+    def population(self):
+        pos = np.empty((self.cfg.ps, self.cfg.dim))
+        fit = np.empty(self.cfg.ps)
+        _lib.check(self.lib.apo_run_population(self.handle, pos.ctypes.data, fit.ctypes.data, 1),
+                   "apo_run_population")
+        return pos, fit
+
+    def close(self):
+        if self.handle:
+            self.lib.apo_run_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _batch_fits(cfg: ApoConfig) -> bool:
+    return int(_lib.require_cuda().apo_run_batch_max_elems(cfg.ps, cfg.dim)) > 0
+
+
+def run(cfg: ApoConfig, objective, mode: Optional[EngineMode] = None, backend: Optional[str] = None) -> RunResult:
+    """Full run: initialise, then iterate within the iteration / evaluation budget (engine.py:175-212)."""
+    mode = mode or EngineMode.sequential()
+    obj = resolve_objective(objective)
+    bk = _resolve_backend(obj, backend)
+    workers = resolve_workers(mode, bk)
+    _check(cfg, obj)
+    n_iters = cfg.iterations_within_budget()
+    started = time.perf_counter()
+    if cfg.ps <= BATCH_PS_LIMIT and _batch_fits(cfg):
+        b = run_batch(cfg, [obj], [cfg.seed], want_population=True)
+        seconds = time.perf_counter() - started
+        return RunResult(best_position=b.best_position[0], best_fitness=float(b.best_fitness[0]), trace=b.trace[0],
+                         iterations_run=n_iters, fe_count=cfg.ps * (1 + n_iters), warnings=int(b.warnings[0]),
+                         wall_clock_seconds=seconds, mode=mode.kind, workers=workers, backend=bk.NAME,
+                         config_echo=cfg,
+                         population=Population(b.final_pos[0], b.final_fit[0], iteration=n_iters,
+                                               fe_count=cfg.ps * (1 + n_iters), warnings=int(b.warnings[0])))
+    dr = DeviceRun(cfg, obj)
+    try:
+        dr.initialize()
+        dr.iterate(n_iters)
+        it, fe, warned = dr.counters()
+        trace = dr.trace(it)
+        best_f, best_x, _ = dr.best()
+        pos, fit = dr.population()
+    finally:
+        dr.close()
+    seconds = time.perf_counter() - started
+    return RunResult(best_position=best_x, best_fitness=best_f, trace=trace, iterations_run=it, fe_count=fe,
+                     warnings=warned, wall_clock_seconds=seconds, mode=mode.kind, workers=workers, backend=bk.NAME,
+                     config_echo=cfg,
+                     population=Population(pos, fit, iteration=it, fe_count=fe, warnings=warned))
+
+
+@dataclass
+class BatchResult:
+    """Outcome of ``run_batch``/``run_many``: arrays indexed by run."""
+
+    best_fitness: np.ndarray
+    best_position: np.ndarray
+    trace: Optional[np.ndarray]
+    warnings: np.ndarray
+    final_pos: Optional[np.ndarray] = None
+    final_fit: Optional[np.ndarray] = None
+    seconds: float = 0.0
+    objectives: tuple = ()
+    seeds: tuple = ()
+
+
+def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_trace: bool = True,
+              want_population: bool = False, device_out: bool = False, stream=None) -> BatchResult:
+    """Independent runs (same ps/dim/bounds/T), one CTA each, on the current GPU."""
+    import torch
+
+    lib = _lib.require_cuda()
+    objs = [resolve_objective(o) for o in objectives]
+    if len(objs) != len(seeds):
+        raise ValueError("one objective per seed")
+    for o in objs:
+        _check(cfg, o)
+    if not _batch_fits(cfg):
+        raise ValueError(f"ps*dim = {cfg.ps * cfg.dim} does not fit the shared-memory batch kernel")
+    n = len(objs)
+    dev = _dev()
+    n_iters = cfg.iterations_within_budget()
+    descs = (_lib.apo_objective * n)()
+    for k, o in enumerate(objs):
+        descs[k] = device_objective(o, cfg.dim).struct
+    seeds_t = torch.as_tensor(np.array([int(s) for s in seeds], dtype=np.uint64).view(np.int64), device=dev)
+    sched = torch.as_tensor(np.array(schedule_table(cfg.max_iterations))
+                            if cfg.max_iterations else np.zeros(3), device=dev)
+    pdr = torch.as_tensor(np.array(p_dr_table(cfg.ps)), device=dev)
+    best_fit = torch.empty(n, dtype=torch.float64, device=dev)
+    best_pos = torch.empty((n, cfg.dim), dtype=torch.float64, device=dev)
+    trace = torch.empty((n, n_iters + 1), dtype=torch.float64, device=dev) if want_trace else None
+    fpos = torch.empty((n, cfg.ps, cfg.dim), dtype=torch.float64, device=dev) if want_population else None
+    ffit = torch.empty((n, cfg.ps), dtype=torch.float64, device=dev) if want_population else None
+    warn = torch.zeros(n, dtype=torch.int64, device=dev)
+    t0 = time.perf_counter()
+    _lib.check(lib.apo_run_batch(n, _lib.ptr(seeds_t), descs, cfg.ps, cfg.dim, cfg.max_iterations, n_iters,
+                                 cfg.neighbor_pairs, cfg.pf_max, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,
+                                 _lib.ptr(sched), _lib.ptr(pdr), _lib.ptr(best_fit), _lib.ptr(best_pos),
+                                 _lib.ptr(trace), _lib.ptr(fpos), _lib.ptr(ffit), _lib.ptr(warn),
+                                 _lib.stream_handle(stream)), "apo_run_batch")
+    if device_out:
+        return BatchResult(best_fit, best_pos, trace, warn, fpos, ffit, 0.0, tuple(o.name for o in objs),
+                           tuple(seeds))
+
+    def host(t):
+        return None if t is None else t.cpu().numpy()
+
+    res = BatchResult(host(best_fit), host(best_pos), host(trace), host(warn), host(fpos), host(ffit), 0.0,
+                      tuple(o.name for o in objs), tuple(seeds))
+    res.seconds = time.perf_counter() - t0
+    return res
+
+
+def run_many(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_trace: bool = False,
+             group=None) -> BatchResult:
+    """Seeds x objectives sharded across the ranks of torch.distributed (if initialised).
+
+    Run k goes to rank k % world_size; there is no collective while runs
+    execute -- one all-gather of the per-run results at the end.  Results
+    are identical for any world size (every draw is keyed by seed, not by
+    placement).
+    """
+    import torch
+    import torch.distributed as dist
+
+    objs = [resolve_objective(o) for o in objectives]
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    mine = list(range(rank, len(objs), world))
+    local = run_batch(cfg, [objs[k] for k in mine], [seeds[k] for k in mine], want_trace=want_trace) if mine else None
+    if world == 1:
+        return local
+    n_iters = cfg.iterations_within_budget()
+    width = 2 + cfg.dim + (n_iters + 1 if want_trace else 0)
+    rows = np.full((len(mine), width), np.nan)
+    for a, k in enumerate(mine):
+        rows[a, 0] = k
+        rows[a, 1] = local.best_fitness[a]
+        rows[a, 2:2 + cfg.dim] = local.best_position[a]
+        if want_trace:
+            rows[a, 2 + cfg.dim:] = local.trace[a]
+    per = -(-len(objs) // world)
+    buf = np.full((per, width + 1), np.nan)
+    buf[:len(mine), :width] = rows
+    buf[:len(mine), width] = local.warnings if local is not None else 0
+    backend = dist.get_backend(group)
+    tdev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.as_tensor(buf, device=tdev)
+    gathered = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(gathered, t, group=group)
+    allrows = np.concatenate([g.cpu().numpy() for g in gathered])
+    allrows = allrows[~np.isnan(allrows[:, 0])]
+    allrows = allrows[np.argsort(allrows[:, 0], kind="stable")]
+    return BatchResult(best_fitness=allrows[:, 1].copy(), best_position=allrows[:, 2:2 + cfg.dim].copy(),
+                       trace=allrows[:, 2 + cfg.dim:width].copy() if want_trace else None,
+                       warnings=allrows[:, width].astype(np.int64), objectives=tuple(o.name for o in objs),
+                       seeds=tuple(seeds))
+
+
+# ---------------------------------------------------------------------------
+# seed-sweep benchmark (engine.py:215-284)
+
+
+@dataclass
+class ModeAggregate:
+    mode: str
+    workers: int
+    best_fitness: list
+    seconds: list
+    results: list = field(repr=False, default_factory=list)
+
+    @property
+    def avg_best_fitness(self) -> float:
+        return fmean(self.best_fitness)
+
+    @property
+    def avg_seconds(self) -> float:
+        return fmean(self.seconds)
+
+
+@dataclass
+class BenchmarkResult:
+    objective_name: str
+    runs: int
+    base_seed: int
+    per_mode: dict
+    speedup: Optional[float]
+
+    def aggregate(self, kind: str) -> ModeAggregate:
+        return self.per_mode[kind]
+
+
+def benchmark(cfg: ApoConfig, objective, runs: int, modes: Sequence[EngineMode] = (),
+              backend: Optional[str] = None) -> BenchmarkResult:
+    if runs < 1:
+        raise ValueError(f"runs must be >= 1, got {runs}")
+    obj = resolve_objective(objective)
+    mode_list = list(modes) or [EngineMode.sequential(), EngineMode.parallel()]
+    per_mode: dict = {}
+    for mode in mode_list:
+        if mode.kind in per_mode:
+            raise ValueError(f"duplicate mode {mode.kind!r} in benchmark request")
+        agg = ModeAggregate(mode.kind, 0, [], [])
+        for r in range(runs):
+            res = run(replace(cfg, seed=cfg.seed + r), obj, mode, backend=backend)
+            agg.workers = res.workers
+            agg.best_fitness.append(res.best_fitness)
+            agg.seconds.append(res.wall_clock_seconds)
+            agg.results.append(res)
+        per_mode[mode.kind] = agg
+    speedup = None
+    if SEQUENTIAL in per_mode and PARALLEL in per_mode:
+        par = per_mode[PARALLEL].avg_seconds
+        speedup = per_mode[SEQUENTIAL].avg_seconds / par if par > 0.0 else math.inf
+    return BenchmarkResult(obj.name, runs, cfg.seed, per_mode, speedup)

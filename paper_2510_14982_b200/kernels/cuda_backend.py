@@ -1,0 +1,76 @@
+"""The "cuda" backend: the reference's run_updates protocol on the B200.
+
+Module protocol (kernels/numba_backend.py:26,48,323 of the reference):
+``NAME``, ``max_workers()`` and ``run_updates(positions, fitness, in_dr,
+cfg, objective, iteration, key_iteration, parallel, workers)`` returning
+``(new_positions, new_fitness, accepted, warning_count)``.  Inputs are read
+only.  numpy inputs give numpy outputs (host<->device copies included);
+CUDA tensors stay on the device.  ``parallel``/``workers`` are accepted for
+signature compatibility: results never depend on them.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .. import _lib
+from ..core import ApoConfig, iteration_scalars, p_dr_table
+from ..objectives import EXTERNAL, Objective, device_objective
+
+NAME = "cuda"
+
+
+def max_workers() -> int:
+    """Visible CUDA devices (the reference reports CPU threads)."""
+    try:
+        return max(1, int(_lib.load().apo_device_count()))
+    except Exception:
+        return 1
+
+
+_PDR_DEV: dict = {}
+
+
+def p_dr_device(ps: int, device):
+    import torch
+
+    key = (ps, str(device))
+    t = _PDR_DEV.get(key)
+    if t is None:
+        t = torch.as_tensor(np.array(p_dr_table(ps)), device=device)
+        _PDR_DEV[key] = t
+    return t
+
+
+def run_updates(positions, fitness, in_dr, cfg: ApoConfig, objective: Objective, iteration: int,
+                key_iteration: int, parallel: bool = False, workers: int = 1):
+    import torch
+
+    if objective.code == EXTERNAL:
+        raise ValueError("the cuda backend cannot call external objective functions")
+    lib = _lib.require_cuda()
+    host = not isinstance(positions, torch.Tensor)
+    dev = torch.device("cuda", torch.cuda.current_device()) if host else positions.device
+    pos = torch.as_tensor(np.ascontiguousarray(positions, dtype=np.float64) if host else positions,
+                          dtype=torch.float64, device=dev).contiguous()
+    fit = torch.as_tensor(np.ascontiguousarray(fitness, dtype=np.float64) if host else fitness,
+                          dtype=torch.float64, device=dev).contiguous()
+    dr = torch.as_tensor(np.ascontiguousarray(in_dr, dtype=np.uint8) if host else in_dr, device=dev)
+    dr = dr.to(torch.uint8).contiguous()
+    ps, dim = pos.shape
+    if fit.shape != (ps,) or dr.shape != (ps,):
+        raise ValueError("fitness and in_dr must have one entry per row of positions")
+    out_pos = torch.empty_like(pos)
+    out_fit = torch.empty_like(fit)
+    acc = torch.empty(ps, dtype=torch.uint8, device=dev)
+    warn = torch.zeros(1, dtype=torch.int64, device=dev)
+    p_ah, f_mult, decay = iteration_scalars(iteration, cfg.max_iterations)
+    dobj = device_objective(objective, dim)
+    rc = lib.apo_run_updates_obj(
+        _lib.ptr(pos), _lib.ptr(fit), _lib.ptr(dr), _lib.ptr(out_pos), _lib.ptr(out_fit), _lib.ptr(acc), None,
+        ps, dim, cfg.seed, key_iteration, cfg.neighbor_pairs, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,
+        p_ah, f_mult, decay, dobj.ref, _lib.ptr(p_dr_device(ps, dev)), _lib.ptr(warn), _lib.stream_handle())
+    _lib.check(rc, "apo_run_updates")
+    if host:
+        return out_pos.cpu().numpy(), out_fit.cpu().numpy(), acc.cpu().numpy().astype(bool), int(warn.item())
+    return out_pos, out_fit, acc.bool(), int(warn.item())
