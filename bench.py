@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""bench.py -- APO population-update throughput on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c4|c2]
+
+A "step" is one APO iteration (stable sort -> coordinator draws -> fused
+update of every protozoon) over the resident population.  Headline
+workload (BASELINE.json config 4 at one GPU): ps = 1,000,000, D = 100,
+objective ``--objective`` (default rosenbrock; F6/F10 are CEC2022 names
+when built), 800 MB population in HBM (> L2, so no flush is needed).
+Multi-GPU (torchrun): every rank runs its own independent population
+(seed = rank), no collective on the data path -> weak scaling; time is the
+max over ranks of CUDA-event time.
+
+``--impl reference`` times the CPU restatement of the reference iteration
+(oracle/, bit-identical to the reference's numba path) on this host's
+cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "protozoa-evals/sec"
+UNIT = "evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2"])
+    ap.add_argument("--objective", default="rosenbrock")
+    ap.add_argument("--ps", type=int, default=1_000_000)
+    ap.add_argument("--dim", type=int, default=100)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-suite", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+def dist_setup(backend):
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return out
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        out.update(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                   reasons=reasons, samples=len(rows))
+        return out
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def profile_traffic(workload: str, objective: str):
+    """dram bytes per update launch from the committed ncu --set full capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(f"{workload}:{objective}")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+
+
+def op_mix(seed: int, key_iteration: int, ps: int, p_ah: float, in_dr: np.ndarray) -> float:
+    """Exact autotroph fraction of one iteration (population independent)."""
+    from paper_2510_14982_b200 import rng
+
+    i = np.arange(1, ps + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = rng._mix_vec(np.uint64(rng.H0) ^ np.uint64(seed))
+        h = rng._mix_vec(np.uint64(h) ^ np.uint64(key_iteration))
+        base = rng._mix_vec(np.uint64(h) ^ i)
+        u = (rng._mix_vec(base) >> np.uint64(11)).astype(np.float64) * rng.INV_2_53
+    return float(np.count_nonzero((~in_dr) & (u < p_ah))) / ps
+
+
+def bytes_per_eval(dim: int, p_auto: float, npairs: int = 1) -> float:
+    return 8.0 * dim * (2.0 + p_auto * (1 + 2 * npairs)) + 32.0
+
+
+# ---------------------------------------------------------------------------
+
+
+def bench_ours(args, rank, world, local):
+    import torch
+
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200 import _lib
+    from paper_2510_14982_b200.core import iteration_scalars
+    from paper_2510_14982_b200.engine import DeviceRun
+
+    torch.cuda.set_device(local)
+    ps, dim, K, W = args.ps, args.dim, args.steps, args.warmup
+    T = max(100, K + W)
+    obj = pz.get_objective(args.objective)
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=T, seed=rank)
+    run = DeviceRun(cfg, obj)
+    run.initialize()
+    run.iterate(W)
+    torch.cuda.synchronize()
+    run.profile(True)
+    clocks = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run.iterate(K)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    upd_ms, launches = run.profile_read()
+    max_ms = max_over_ranks(ms, world)
+    value = world * ps * K / (max_ms / 1e3)
+    # algorithmic bytes of the timed launches (rank 0's population; ranks are statistically identical)
+    dev = torch.device("cuda", local)
+    in_dr = torch.empty(ps, dtype=torch.uint8, device=dev)
+    total_bytes = 0.0
+    p_autos = []
+    for t in range(W, W + K):
+        _lib.check(_lib.load().apo_select_dr(cfg.seed, t + 1, ps, cfg.pf_max, _lib.ptr(in_dr), None,
+                                             _lib.stream_handle()))
+        p_auto = op_mix(cfg.seed, t + 1, ps, iteration_scalars(t, T)[0], in_dr.cpu().numpy().astype(bool))
+        p_autos.append(p_auto)
+        total_bytes += ps * bytes_per_eval(dim, p_auto, cfg.neighbor_pairs)
+    per_launch = total_bytes / K
+    kern_s = upd_ms / 1e3 / max(launches, 1)
+    peaks, peak_kind = measured_peaks()
+    achieved = per_launch / kern_s / 1e9
+    traffic = profile_traffic("c4", args.objective)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                "peak_source": peak_kind, "kernel": "k_update<true>",
+                "kernel_ms_avg": round(upd_ms / max(launches, 1), 4),
+                "kernel_share_of_step": round(upd_ms / ms, 4),
+                "bytes_per_launch": per_launch, "bytes_per_eval": round(per_launch / ps, 1),
+                "p_auto_mean": round(float(np.mean(p_autos)), 4)}
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (keyed-hash initial population, seed = rank)",
+        "config": {"workload": f"C4: single population ps={ps} D={dim} objective={args.objective}"
+                               + (" (stand-in for CEC2022 F6/F10)" if args.objective in pz.FUNCTION_NAMES else ""),
+                   "ps": ps, "dim": dim, "iterations_per_step": 1, "max_iterations": T,
+                   "l2": "inputs larger than L2 (800 MB population)",
+                   "parallelism": f"independent runs x{world}" if world > 1 else "single GPU",
+                   "rng": "keyed fmix64 (bit-exact with the reference)"},
+        "roofline": roofline,
+        "clocks": clk,
+        # my kernels per iteration: k_make_keys, k_dr_draw, k_dr_resolve, k_update (+ CUB radix-sort passes)
+        "gpu_launches": 4 * K,
+    }
+    run.close()
+    del run
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        result["e2e"] = bench_e2e(cfg, obj, K, rank, world)
+    if not args.no_suite and rank == 0:
+        result["suite_c2"] = bench_suite(world)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(cfg, args.objective)
+    return result
+
+
+def bench_e2e(cfg, obj, K, rank, world):
+    """Same metric through the public API with HOST buffers: pz.step(Population) per iteration."""
+    import torch
+
+    import paper_2510_14982_b200 as pz
+
+    pop = pz.initialize(cfg, obj)
+    pop = pz.step(pop, cfg, obj, 0)
+    n = max(1, min(K, 3))
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for t in range(1, n + 1):
+        pop = pz.step(pop, cfg, obj, t)
+    torch.cuda.synchronize()
+    dt = max_over_ranks(time.perf_counter() - t0, world)
+    nb = 8 * cfg.ps * cfg.dim + 8 * cfg.ps
+    return {"value": world * cfg.ps * n / dt, "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+            "steps": n, "api": "paper_2510_14982_b200.step(Population numpy) -> Population numpy"}
+
+
+def bench_suite(world):
+    """BASELINE config 2 shape: 360 independent runs (D=20, ps=100, 1000 iterations), one CTA per run."""
+    import torch
+
+    import paper_2510_14982_b200 as pz
+
+    cfg = pz.ApoConfig(ps=100, dim=20, bounds=pz.Bounds(-100.0, 100.0, 20), max_iterations=1000)
+    names = [n for n in ("sphere", "bent_cigar", "high_conditioned_elliptic", "hgbat", "rosenbrock", "griewank")
+             for _ in range(60)]
+    seeds = list(range(len(names)))
+    pz.run_batch(cfg, names[:16], seeds[:16], want_trace=False, device_out=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pz.run_batch(cfg, names, seeds, want_trace=False, device_out=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    evals = len(names) * cfg.ps * cfg.max_iterations
+    return {"value": evals / (ms / 1e3), "unit": UNIT, "ms": ms, "runs": len(names),
+            "workload": "C2 shape: 6 reference functions x 60 seeds, D=20, ps=100, T=1000 (CEC2022 F1-F12 pending)",
+            "gpus": 1}
+
+
+def cpu_baseline(cfg, objective, max_seconds=25.0):
+    """The oracle's reference iteration (oracle.step, bit-identical to the reference) on all host cores."""
+    import oracle
+
+    nthreads = os.cpu_count() or 1
+    pos, fit = oracle.initialize(cfg.seed, cfg.ps, cfg.dim, cfg.bounds.lower, cfg.bounds.upper, objective)
+    done = 0
+    t0 = time.perf_counter()
+    while True:
+        pos, fit, _, _ = oracle.step(pos, fit, seed=cfg.seed, iteration=done, max_iterations=cfg.max_iterations,
+                                     name=objective, lower=cfg.bounds.lower, upper=cfg.bounds.upper,
+                                     pf_max=cfg.pf_max, nthreads=nthreads)
+        done += 1
+        if time.perf_counter() - t0 > max_seconds / 2 or done >= 5:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": cfg.ps * done / dt, "unit": UNIT, "cores": nthreads, "kind": "port",
+            "sample": f"{done} full iterations of ps={cfg.ps} D={cfg.dim} {objective} "
+                      "(oracle.step: stable sort + gather + coordinator + OpenMP update)",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def bench_reference(args, rank, world):
+    """CPU reference arm: rank 0 times oracle.step on the same workload with every host core."""
+    if rank != 0:
+        return None
+    import oracle
+    import paper_2510_14982_b200 as pz
+
+    ps, dim, K, W = args.ps, args.dim, args.steps, args.warmup
+    T = max(100, K + W)
+    nthreads = os.cpu_count() or 1
+    pos, fit = oracle.initialize(0, ps, dim, -100.0, 100.0, args.objective)
+    step_args = dict(seed=0, max_iterations=T, name=args.objective, lower=-100.0, upper=100.0, nthreads=nthreads)
+    t0 = time.perf_counter()
+    for t in range(W):
+        pos, fit, _, _ = oracle.step(pos, fit, iteration=t, **step_args)
+    t_warm = (time.perf_counter() - t0) / max(W, 1)
+    budget = 150.0
+    k_run = max(1, min(K, int(budget / max(t_warm, 1e-3))))
+    t0 = time.perf_counter()
+    for t in range(W, W + k_run):
+        pos, fit, _, _ = oracle.step(pos, fit, iteration=t, **step_args)
+    dt = time.perf_counter() - t0
+    value = ps * k_run / dt
+    sample = (f"{k_run} of {K} requested full iterations (budget {budget:.0f} s) of ps={ps} D={dim} "
+              f"{args.objective} via oracle.step")
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k_run, "warmup": W,
+        "ms_per_step": dt * 1e3 / k_run, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"C4: single population ps={ps} D={dim} objective={args.objective}"
+                               + (" (stand-in for CEC2022 F6/F10)" if args.objective in pz.FUNCTION_NAMES else ""),
+                   "ps": ps, "dim": dim, "iterations_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port", "sample": sample,
+                         "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        res = bench_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    rank, world, local = dist_setup("nccl")
+    if args.workload == "c2":
+        import torch
+
+        torch.cuda.set_device(local)
+        res = bench_suite(world)
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, **res, "n_gpus": world, "steps": 1, "warmup": 1}), flush=True)
+        return
+    res = bench_ours(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

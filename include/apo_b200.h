@@ -128,6 +128,11 @@ int apo_run_population(apo_run *run, double *positions, double *fitness, int is_
 int apo_run_best(apo_run *run, double *best_fitness_host, double *best_position_host, int64_t *best_row_host);
 int apo_run_counters(apo_run *run, int64_t *iterations_run, int64_t *fe_count, int64_t *warnings);
 int apo_run_destroy(apo_run *run);
+/* Timing hook: when enabled, CUDA events on the run's stream bracket every
+ * fused update launch; _read returns their summed duration (ms) and count
+ * since the last apo_run_profile call. */
+int apo_run_profile(apo_run *run, int enable);
+int apo_run_profile_read(apo_run *run, double *update_ms_host, int64_t *launches_host);
 
 /*
  * Many independent small runs, one CTA per run, the whole run resident in

@@ -99,6 +99,8 @@ PROTOTYPES = {
     "apo_run_best": (_INT, [_P, _P, _P, C.POINTER(C.c_int64)]),
     "apo_run_counters": (_INT, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "apo_run_destroy": (_INT, [_P]),
+    "apo_run_profile": (_INT, [_P, _INT]),
+    "apo_run_profile_read": (_INT, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "apo_run_batch": (_INT, [_I, _P, C.POINTER(apo_objective), _I, _I, _I, _I, _I, _D, _D, _D, _D, _P, _P, _P, _P,
                              _P, _P, _P, _P, _P]),
     "apo_run_batch_max_elems": (_I, [_I, _I]),

@@ -601,6 +601,9 @@ struct apo_run {
     unsigned long long* warn;
     int64_t iters;
     bool initialized;
+    // optional CUDA-event timing of the fused update launch (bench.py roofline)
+    bool profile;
+    std::vector<cudaEvent_t> prof_events;
 };
 
 extern "C" {
@@ -788,6 +791,7 @@ int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iteration
     r->cur = 0;
     r->iters = 0;
     r->initialized = false;
+    r->profile = false;
     r->sched.assign(sched_host, sched_host + 3 * max_iterations);
     r->dr_cap = (int64_t)ceil((double)ps * pf_max) + 1;
     const size_t rows = 8 * (size_t)ps * (size_t)r->ld;
@@ -885,10 +889,19 @@ int apo_run_iterate(apo_run* r, int64_t n) {
         P.p_ah = r->sched[3 * t];
         P.f_mult = r->sched[3 * t + 1];
         P.decay = r->sched[3 * t + 2];
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        if (r->profile) {
+            for (auto& e : ev) {
+                APO_CUDA(cudaEventCreate(&e));
+                r->prof_events.push_back(e);
+            }
+            APO_CUDA(cudaEventRecord(ev[0], st));
+        }
         if (int rc = launch_update(true, P, r->obj, r->pos[r->cur], r->fit[r->cur], r->order, nullptr, r->dr_bits,
                                    r->p_dr, r->pos[r->cur ^ 1], r->fit[r->cur ^ 1], nullptr, nullptr, r->warn,
                                    r->trace_keys + t + 1, st))
             return rc;
+        if (r->profile) APO_CUDA(cudaEventRecord(ev[1], st));
         r->cur ^= 1;
         r->iters++;
     }
@@ -960,8 +973,36 @@ int apo_run_counters(apo_run* r, int64_t* iterations_run, int64_t* fe_count, int
     return APO_OK;
 }
 
+static void clear_profile(apo_run* r) {
+    for (cudaEvent_t e : r->prof_events) cudaEventDestroy(e);
+    r->prof_events.clear();
+}
+
+int apo_run_profile(apo_run* r, int enable) {
+    APO_CHECK(r, "run is NULL");
+    APO_CUDA(cudaStreamSynchronize(r->stream));
+    clear_profile(r);
+    r->profile = enable != 0;
+    return APO_OK;
+}
+
+int apo_run_profile_read(apo_run* r, double* update_ms_host, int64_t* launches_host) {
+    APO_CHECK(r, "run is NULL");
+    APO_CUDA(cudaStreamSynchronize(r->stream));
+    double total = 0.0;
+    for (size_t k = 0; k + 1 < r->prof_events.size(); k += 2) {
+        float ms = 0.f;
+        APO_CUDA(cudaEventElapsedTime(&ms, r->prof_events[k], r->prof_events[k + 1]));
+        total += ms;
+    }
+    if (update_ms_host) *update_ms_host = total;
+    if (launches_host) *launches_host = (int64_t)(r->prof_events.size() / 2);
+    return APO_OK;
+}
+
 int apo_run_destroy(apo_run* r) {
     if (!r) return APO_OK;
+    clear_profile(r);
     void* bufs[] = {r->pos[0], r->pos[1], r->fit[0], r->fit[1], r->order, r->keys_in, r->keys_out, r->vals_in,
                     r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn};
     for (void* b : bufs)

@@ -213,6 +213,15 @@ class DeviceRun:
                    "apo_run_population")
         return pos, fit
 
+    def profile(self, enable: bool = True):
+        _lib.check(self.lib.apo_run_profile(self.handle, 1 if enable else 0), "apo_run_profile")
+
+    def profile_read(self):
+        """(summed ms, launches) of the fused update kernel since profile()."""
+        ms, n = C.c_double(), C.c_int64()
+        _lib.check(self.lib.apo_run_profile_read(self.handle, C.byref(ms), C.byref(n)), "apo_run_profile_read")
+        return ms.value, n.value
+
     def close(self):
         if self.handle:
             self.lib.apo_run_destroy(self.handle)
