@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "apo_b200.h"
+#include "apo_group.cuh"
 #include "apo_update.cuh"
 
 using namespace apo;
@@ -142,6 +143,52 @@ __global__ void __launch_bounds__(kThreads) k_update(IterParams P, ObjDesc O, co
         const unsigned long long k = sort_key(res.fitness);
         my_min = k < my_min ? k : my_min;
         my_warn += res.warned ? 1u : 0u;
+    }
+    if (lane == 0) {
+        red_min[warp] = my_min;
+        red_warn[warp] = my_warn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = ~0ull;
+        unsigned w = 0;
+        for (int k = 0; k < nwarps; k++) {
+            m = red_min[k] < m ? red_min[k] : m;
+            w += red_warn[k];
+        }
+        if (trace_key && m != ~0ull) atomicMin(trace_key, m);
+        if (warn_count && w) atomicAdd(warn_count, (unsigned long long)w);
+    }
+}
+
+// Group path (dim <= 256): one warp per 32 consecutive ranks, see apo_group.cuh.
+template <bool INDIRECT, int MAXC>
+__global__ void __launch_bounds__(kThreads) k_update_group(
+    IterParams P, ObjDesc O, const double* __restrict__ pos, const double* __restrict__ fit,
+    const int* __restrict__ order, const uint8_t* __restrict__ in_dr_bytes, const unsigned* __restrict__ in_dr_bits,
+    const double* __restrict__ p_dr, double* __restrict__ out_pos, double* __restrict__ out_fit,
+    uint8_t* __restrict__ out_acc, uint8_t* __restrict__ out_warn, unsigned long long* __restrict__ warn_count,
+    unsigned long long* __restrict__ trace_key) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long red_min[32];
+    __shared__ unsigned red_warn[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const GroupScratch g = group_scratch(smem + (size_t)warp * group_scratch_bytes(P.dim), P.dim);
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    const int ngroups = (P.ps + 31) >> 5;
+    for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
+        const int i0 = grp * 32 + 1;
+        const int n = min(32, P.ps - grp * 32);
+        if (INDIRECT) {
+            const OrderedSlots R{pos, fit, order, P.ld};
+            update_group<MAXC>(P, O, R, i0, n, in_dr_bytes, in_dr_bits, p_dr, out_pos, out_fit, true, out_acc,
+                               out_warn, g, lane, my_min, my_warn);
+        } else {
+            const DenseSlots R{pos, fit, P.ld};
+            update_group<MAXC>(P, O, R, i0, n, in_dr_bytes, in_dr_bits, p_dr, out_pos, out_fit, false, out_acc,
+                               out_warn, g, lane, my_min, my_warn);
+        }
     }
     if (lane == 0) {
         red_min[warp] = my_min;
@@ -329,6 +376,10 @@ struct BatchLayout {
     size_t pos0, pos1, fit0, fit1, keys, order, rankof, newrank, chead, cprev, crj, cbits, warps, total;
 };
 
+__host__ __device__ inline size_t batch_warp_bytes(int dim) {
+    return dim <= kGroupMaxDim ? group_scratch_bytes(dim) : warp_scratch_bytes(dim);
+}
+
 __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int nwarps) {
     BatchLayout L;
     size_t o = 0;
@@ -349,11 +400,13 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
     L.cprev = take(4 * (size_t)ps);
     L.crj = take(4 * (size_t)ps);
     L.cbits = take(4 * (size_t)((ps + 31) / 32));
-    L.warps = take(warp_scratch_bytes(dim) * (size_t)nwarps);
+    L.warps = take(batch_warp_bytes(dim) * (size_t)nwarps);
     L.total = o;
     return L;
 }
 
+// MAXC >= 0: group path (apo_group.cuh); MAXC < 0: warp-per-protozoon (dim > 256).
+template <int MAXC>
 __global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ unsigned long long red_min[32];
@@ -373,7 +426,9 @@ __global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
     cs.prev = reinterpret_cast<int*>(smem + L.cprev);
     cs.rj = reinterpret_cast<int*>(smem + L.crj);
     cs.bits = reinterpret_cast<unsigned*>(smem + L.cbits);
-    const WarpScratch ws = warp_scratch(smem + L.warps + (size_t)warp * warp_scratch_bytes(dim), dim);
+    unsigned char* wbase = smem + L.warps + (size_t)warp * batch_warp_bytes(dim);
+    const GroupScratch g = group_scratch(wbase, dim);
+    const WarpScratch ws = MAXC >= 0 ? g.ws : warp_scratch(wbase, dim);
     const uint64_t seed = A.seeds[run];
     const ObjDesc O = A.objs[run];
     double* trace = A.trace ? A.trace + (size_t)run * (A.n_iters + 1) : nullptr;
@@ -446,21 +501,33 @@ __global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
         P.p_ah = A.sched[3 * t];
         P.f_mult = A.sched[3 * t + 1];
         P.decay = A.sched[3 * t + 2];
-        const OrderedRows R{pos[cur], fit[cur], order, ld};
         const int nxt = cur ^ 1;
         my_min = ~0ull;
         unsigned my_warn = 0;
-        for (int r0 = warp; r0 < ps; r0 += nwarps) {
-            const bool dr = ((cs.bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0;
-            const int slot = order[r0];
-            const UpdateResult res = update_protozoon(P, O, R, r0 + 1, dr, dr ? A.p_dr[r0] : 0.0,
-                                                      pos[nxt] + (size_t)slot * ld, ws, lane);
-            if (lane == 0) {
-                fit[nxt][slot] = res.fitness;
-                const unsigned long long k = sort_key(res.fitness);
-                keys[slot] = k;
-                my_min = k < my_min ? k : my_min;
-                my_warn += res.warned ? 1u : 0u;
+        if constexpr (MAXC >= 0) {
+            const OrderedSlots R{pos[cur], fit[cur], order, ld};
+            const int G = min(32, (ps + nwarps - 1) / nwarps);
+            for (int q = warp; q * G < ps; q += nwarps) {
+                const int i0 = q * G + 1;
+                update_group<MAXC>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr, pos[nxt], fit[nxt],
+                                   true, nullptr, nullptr, g, lane, my_min, my_warn);
+            }
+            __syncthreads();
+            for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) keys[sl] = sort_key(fit[nxt][sl]);
+        } else {
+            const OrderedRows R{pos[cur], fit[cur], order, ld};
+            for (int r0 = warp; r0 < ps; r0 += nwarps) {
+                const bool dr = ((cs.bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0;
+                const int slot = order[r0];
+                const UpdateResult res = update_protozoon(P, O, R, r0 + 1, dr, dr ? A.p_dr[r0] : 0.0,
+                                                          pos[nxt] + (size_t)slot * ld, ws, lane);
+                if (lane == 0) {
+                    fit[nxt][slot] = res.fitness;
+                    const unsigned long long k = sort_key(res.fitness);
+                    keys[slot] = k;
+                    my_min = k < my_min ? k : my_min;
+                    my_warn += res.warned ? 1u : 0u;
+                }
             }
         }
         if (lane == 0) {
@@ -505,6 +572,26 @@ int launch_update(bool indirect, const IterParams& P, const ObjDesc& O, const do
                   const int* order, const uint8_t* in_dr_bytes, const unsigned* in_dr_bits, const double* p_dr,
                   double* out_pos, double* out_fit, uint8_t* out_acc, uint8_t* out_warn,
                   unsigned long long* warn_count, unsigned long long* trace_key, cudaStream_t st) {
+    if (P.dim <= kGroupMaxDim) {
+        const size_t smem = group_scratch_bytes(P.dim) * (size_t)kWarps;
+        const void* fn;
+        if (P.dim <= 32) fn = indirect ? (const void*)k_update_group<true, 1> : (const void*)k_update_group<false, 1>;
+        else if (P.dim <= 64) fn = indirect ? (const void*)k_update_group<true, 2> : (const void*)k_update_group<false, 2>;
+        else if (P.dim <= 128) fn = indirect ? (const void*)k_update_group<true, 4> : (const void*)k_update_group<false, 4>;
+        else fn = indirect ? (const void*)k_update_group<true, 0> : (const void*)k_update_group<false, 0>;
+        if (int rc = set_smem(fn, smem)) return rc;
+        int per_sm = 1;
+        APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+        if (per_sm < 1) per_sm = 1;
+        const long long need = ((long long)(P.ps + 31) / 32 + kWarps - 1) / kWarps;
+        const long long cap = (long long)per_sm * num_sms();
+        const int grid = (int)(need < cap ? need : cap);
+        void* args[] = {(void*)&P,        (void*)&O,     (void*)&pos,     (void*)&fit,      (void*)&order,
+                        (void*)&in_dr_bytes, (void*)&in_dr_bits, (void*)&p_dr, (void*)&out_pos, (void*)&out_fit,
+                        (void*)&out_acc,  (void*)&out_warn, (void*)&warn_count, (void*)&trace_key};
+        APO_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, st));
+        return APO_OK;
+    }
     const int w = warps_for_dim(P.dim);
     const size_t smem = warp_scratch_bytes(P.dim) * (size_t)w;
     const void* fn = indirect ? (const void*)k_update<true> : (const void*)k_update<false>;
@@ -1064,8 +1151,14 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     A.final_fit = final_fit;
     A.warnings = (long long*)warnings;
     const BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps);
-    if (int rc = set_smem((const void*)k_run_batch, L.total)) return rc;
-    k_run_batch<<<(int)nruns, kThreads, L.total, st>>>(A);
+    const void* fn = dim <= 32    ? (const void*)k_run_batch<1>
+                     : dim <= 64  ? (const void*)k_run_batch<2>
+                     : dim <= 128 ? (const void*)k_run_batch<4>
+                     : dim <= kGroupMaxDim ? (const void*)k_run_batch<0>
+                                           : (const void*)k_run_batch<-1>;
+    if (int rc = set_smem(fn, L.total)) return rc;
+    void* args[] = {(void*)&A};
+    APO_CUDA(cudaLaunchKernel(fn, dim3((unsigned)nruns), dim3(kThreads), args, L.total, st));
     APO_CUDA(cudaGetLastError());
     cudaFreeAsync(d_descs, st);
     return APO_OK;

@@ -29,6 +29,22 @@ struct ObjDesc {
 
 __device__ __forceinline__ double warp_bcast(double v, int src) { return __shfl_sync(0xFFFFFFFFu, v, src); }
 
+// s = 0.0; for d in [from, to): s += t[d]  -- strictly left to right, with
+// 16-byte shared loads (t must be 16-byte aligned).
+__device__ __forceinline__ double seq_sum(const double* t, int from, int to) {
+    double s = 0.0;
+    int d = from;
+    if ((d & 1) && d < to) s += t[d++];
+#pragma unroll 4
+    for (; d + 1 < to; d += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(t + d);
+        s += v.x;
+        s += v.y;
+    }
+    if (d < to) s += t[d];
+    return s;
+}
+
 // c: candidate [dim] (shared), t: scratch [dim] (shared).  Returns the
 // fitness on every lane.
 __device__ inline double eval_warp(const ObjDesc& O, const double* c, double* t, int dim, int lane) {
@@ -37,39 +53,24 @@ __device__ inline double eval_warp(const ObjDesc& O, const double* c, double* t,
     case OBJ_SPHERE:
         for (int d = lane; d < dim; d += 32) t[d] = c[d] * c[d];
         __syncwarp();
-        if (lane == 0) {
-            double s = 0.0;
-            for (int d = 0; d < dim; d++) s += t[d];
-            f = s;
-        }
+        if (lane == 0) f = seq_sum(t, 0, dim);
         break;
     case OBJ_BENT_CIGAR:
         for (int d = lane; d < dim; d += 32) t[d] = c[d] * c[d];
         __syncwarp();
-        if (lane == 0) {
-            double s = 0.0;
-            for (int d = 1; d < dim; d++) s += t[d];
-            f = t[0] + 1e6 * s;
-        }
+        if (lane == 0) f = t[0] + 1e6 * seq_sum(t, 1, dim);
         break;
     case OBJ_ELLIPTIC:
         for (int d = lane; d < dim; d += 32) t[d] = (O.table[d] * c[d]) * c[d];
         __syncwarp();
-        if (lane == 0) {
-            double s = 0.0;
-            for (int d = 0; d < dim; d++) s += t[d];
-            f = s;
-        }
+        if (lane == 0) f = seq_sum(t, 0, dim);
         break;
     case OBJ_HGBAT:
         for (int d = lane; d < dim; d += 32) t[d] = c[d] * c[d];
         __syncwarp();
         if (lane == 0) {
-            double s1 = 0.0, s2 = 0.0;
-            for (int d = 0; d < dim; d++) {
-                s1 += c[d];
-                s2 += t[d];
-            }
+            const double s1 = seq_sum(c, 0, dim);
+            const double s2 = seq_sum(t, 0, dim);
             f = sqrt(fabs(s2 * s2 - s1 * s1)) + (0.5 * s2 + s1) / (double)dim + 0.5;
         }
         break;
@@ -80,11 +81,7 @@ __device__ inline double eval_warp(const ObjDesc& O, const double* c, double* t,
             t[d] = 100.0 * (a * a) + b * b;
         }
         __syncwarp();
-        if (lane == 0) {
-            double s = 0.0;
-            for (int d = 0; d < dim - 1; d++) s += t[d];
-            f = s;
-        }
+        if (lane == 0) f = seq_sum(t, 0, dim - 1);
         break;
     case OBJ_GRIEWANK:
         // cos through CUDA's libdevice (<= 1-2 ulp); glibc's cos is not

@@ -46,16 +46,19 @@ struct WarpScratch {
 };
 
 __host__ __device__ inline size_t warp_scratch_bytes(int dim) {
+    const size_t d2 = (size_t)((dim + 1) & ~1);
     size_t words = (size_t)(dim + 31) / 32;
-    size_t b = 16 * (size_t)dim + 12 * (size_t)dim + 4 * words + 8 * kMaxCachedPairs + 8 * kMaxCachedPairs;
+    size_t b = 16 * d2 + 12 * (size_t)dim + 4 * words + 8 * kMaxCachedPairs + 8 * kMaxCachedPairs;
     return (b + 15) & ~(size_t)15;
 }
 
+// cand and terms start 16-byte aligned (eval_warp reads them as double2).
 __device__ inline WarpScratch warp_scratch(unsigned char* base, int dim) {
     WarpScratch s;
+    const int d2 = (dim + 1) & ~1;
     s.cand = reinterpret_cast<double*>(base);
-    s.terms = s.cand + dim;
-    s.pw = s.terms + dim;
+    s.terms = s.cand + d2;
+    s.pw = s.terms + d2;
     s.head = reinterpret_cast<int*>(s.pw + kMaxCachedPairs);
     s.prev = s.head + dim;
     s.rj = s.prev + dim;
