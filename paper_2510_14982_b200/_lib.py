@@ -108,9 +108,12 @@ PROTOTYPES = {
 }
 
 
-def load(path: str = LIB_PATH):
-    """dlopen the library and bind every prototype (no device needed)."""
+def load(path: str = None):
+    """dlopen the library and bind every prototype (no device needed).
+
+    APO_LIB overrides the path (used to A/B build variants; never set in tests)."""
     global _lib
+    path = path or os.environ.get("APO_LIB") or LIB_PATH
     with _lock:
         if _lib is not None:
             return _lib

@@ -18,6 +18,22 @@ namespace apo {
 
 constexpr int kGroupMaxDim = 256;  // uint8 permutations
 
+// Terms batch: protozoa whose per-dimension fitness terms are staged in shared
+// memory before 1 lane each folds them sequentially.
+#ifndef APO_LOAD_CHUNKS
+#define APO_LOAD_CHUNKS 4
+#endif
+#ifndef APO_GROUP_BATCH_SMALL_D
+#define APO_GROUP_BATCH_SMALL_D 16
+#endif
+#ifndef APO_GROUP_BATCH_LARGE_D
+#define APO_GROUP_BATCH_LARGE_D 8
+#endif
+__host__ __device__ inline int group_batch(int dim) {
+    return dim <= 64 ? APO_GROUP_BATCH_SMALL_D : APO_GROUP_BATCH_LARGE_D;
+}
+__host__ __device__ inline int group_tstride(int dim) { return dim | 1; }  // odd: conflict-free lane rows
+
 // Per-warp shared scratch of the group path.
 struct GroupScratch {
     unsigned char* perm;  // [32][dp]
@@ -27,32 +43,46 @@ struct GroupScratch {
     double* w;            // [32] pair-0 weight
     int* slot;            // [32][4] own, partner, km, kp slots
     int* op;              // [32]
-    WarpScratch ws;       // cand/terms (+ pair cache for npairs > 1)
-    int dp, words;
+    double* T;            // [batch][tstride] fitness terms
+    WarpScratch ws;       // only ws.pk / ws.pw (pair cache for npairs > 1) are used
+    int dp, words, tstride, batch;
 };
 
-__host__ __device__ inline size_t group_scratch_bytes(int dim) {
-    const size_t dp = (size_t)((dim + 3) & ~3);
+// Layout: [header: scalars, slots, ops, pair cache, mask bits][union: phase-A
+// permutations (32 x dp bytes) | phase-B terms (batch x tstride doubles)].
+// The permutations are dead once phase A ends, so the terms reuse them.
+__host__ __device__ inline size_t group_head_bytes(int dim) {
     const size_t words = (size_t)(dim + 31) / 32;
-    size_t b = 32 * dp + 32 * words * 4 + 32 * 8 * 3 + 32 * 4 * 4 + 32 * 4;
-    b = (b + 15) & ~(size_t)15;
-    return b + warp_scratch_bytes(dim);
+    size_t b = 32 * 8 * 3 + 32 * 4 * 4 + 32 * 4 + 32 * words * 4;
+    b += 8 * 3 * kMaxCachedPairs;
+    return (b + 15) & ~(size_t)15;
+}
+
+__host__ __device__ inline size_t group_scratch_bytes(int dim) {
+    const size_t perm = 32 * (size_t)((dim + 3) & ~3);
+    const size_t terms = 8 * (size_t)group_batch(dim) * (size_t)group_tstride(dim);
+    return group_head_bytes(dim) + ((perm > terms ? perm : terms) + 15) / 16 * 16;
 }
 
 __device__ inline GroupScratch group_scratch(unsigned char* base, int dim) {
     GroupScratch g;
     g.dp = (dim + 3) & ~3;
     g.words = (dim + 31) / 32;
+    g.tstride = group_tstride(dim);
+    g.batch = group_batch(dim);
     g.f = reinterpret_cast<double*>(base);
     g.sgn = g.f + 32;
     g.w = g.sgn + 32;
-    g.slot = reinterpret_cast<int*>(g.w + 32);
+    g.ws.pw = g.w + 32;
+    g.slot = reinterpret_cast<int*>(g.ws.pw + kMaxCachedPairs);
     g.op = g.slot + 128;
-    g.bits = reinterpret_cast<unsigned*>(g.op + 32);
-    g.perm = reinterpret_cast<unsigned char*>(g.bits + 32 * g.words);
-    size_t used = 32 * (size_t)g.dp + 32 * (size_t)g.words * 4 + 32 * 8 * 3 + 32 * 4 * 4 + 32 * 4;
-    used = (used + 15) & ~(size_t)15;
-    g.ws = warp_scratch(base + used, dim);
+    g.ws.pk = g.op + 32;
+    g.bits = reinterpret_cast<unsigned*>(g.ws.pk + 2 * kMaxCachedPairs);
+    g.perm = base + group_head_bytes(dim);
+    g.T = reinterpret_cast<double*>(base + group_head_bytes(dim));
+    g.ws.cand = g.ws.terms = nullptr;
+    g.ws.head = g.ws.prev = g.ws.rj = nullptr;
+    g.ws.bits = nullptr;
     return g;
 }
 
@@ -61,6 +91,9 @@ struct DenseSlots {
     const double* fit;
     int ld;
     __device__ __forceinline__ int slot(int rank1) const { return rank1 - 1; }
+    __device__ __forceinline__ int key(int rank1) const { return rank1 - 1; }
+    __device__ __forceinline__ int slot_of(int key) const { return key; }
+    __device__ __forceinline__ const double* at_key(int key) const { return pos + (size_t)key * ld; }
     __device__ __forceinline__ const double* at(int slot) const { return pos + (size_t)slot * ld; }
     __device__ __forceinline__ double fit_at(int slot) const { return fit[slot]; }
     __device__ __forceinline__ const double* row(int rank1) const { return at(rank1 - 1); }
@@ -73,7 +106,46 @@ struct OrderedSlots {
     const int* order;
     int ld;
     __device__ __forceinline__ int slot(int rank1) const { return order[rank1 - 1]; }
+    __device__ __forceinline__ int key(int rank1) const { return order[rank1 - 1]; }
+    __device__ __forceinline__ int slot_of(int key) const { return key; }
+    __device__ __forceinline__ const double* at_key(int key) const { return pos + (size_t)key * ld; }
     __device__ __forceinline__ const double* at(int slot) const { return pos + (size_t)slot * ld; }
+    __device__ __forceinline__ double fit_at(int slot) const { return fit[slot]; }
+    __device__ __forceinline__ const double* row(int rank1) const { return at(order[rank1 - 1]); }
+    __device__ __forceinline__ double fitness(int rank1) const { return fit[order[rank1 - 1]]; }
+};
+
+// HBM-resident population with two row buffers per slot: sel[slot] says which
+// buffer holds the current row.  A candidate is written to the other buffer;
+// acceptance just flips the slot's selector for the next iteration, so a
+// rejected candidate costs no row copy.
+struct SelSlots {
+    const double* pos0;
+    const double* pos1;
+    const uint8_t* sel;
+    const double* fit;
+    const int* order;
+    int ld;
+    __device__ __forceinline__ int slot(int rank1) const { return order[rank1 - 1]; }
+    // key = slot*2 + selector: resolved once in phase A so phase B row loads
+    // do not wait on the selector load.
+    __device__ __forceinline__ int key(int rank1) const {
+        const int s = order[rank1 - 1];
+        return (s << 1) | (int)sel[s];
+    }
+    __device__ __forceinline__ int slot_of(int key) const { return key >> 1; }
+    __device__ __forceinline__ const double* at_key(int key) const {
+        return ((key & 1) ? pos1 : pos0) + (size_t)(key >> 1) * ld;
+    }
+    __device__ __forceinline__ double* alt_key(int key) const {
+        return const_cast<double*>(((key & 1) ? pos0 : pos1) + (size_t)(key >> 1) * ld);
+    }
+    __device__ __forceinline__ const double* at(int slot) const {
+        return (sel[slot] ? pos1 : pos0) + (size_t)slot * ld;
+    }
+    __device__ __forceinline__ double* alt(int slot) const {
+        return const_cast<double*>((sel[slot] ? pos0 : pos1) + (size_t)slot * ld);
+    }
     __device__ __forceinline__ double fit_at(int slot) const { return fit[slot]; }
     __device__ __forceinline__ const double* row(int rank1) const { return at(order[rank1 - 1]); }
     __device__ __forceinline__ double fitness(int rank1) const { return fit[order[rank1 - 1]]; }
@@ -89,8 +161,8 @@ __device__ inline void group_phase_a(const IterParams& P, const Rows& R, int i, 
     int op;
     if (in_dr) op = (u_dec < p_dr_i) ? OP_DORMANCY : OP_REPRODUCTION;
     else op = (u_dec < P.p_ah) ? OP_AUTOTROPH : OP_HETEROTROPH;
-    int* sl = g.slot + 4 * lane;
-    sl[0] = R.slot(i);
+    int* sl = g.slot + 4 * lane;  // row keys (see SelSlots::key)
+    sl[0] = R.key(i);
     int count = 0;
     if (op == OP_REPRODUCTION) {
         const double sgn = uniform(base, kSlotSign) < 0.5 ? 1.0 : -1.0;
@@ -107,7 +179,7 @@ __device__ inline void group_phase_a(const IterParams& P, const Rows& R, int i, 
                 if (j0 >= i - 1) j0 += 1;
                 partner = j0 + 1;
             }
-            sl[1] = R.slot(partner);
+            sl[1] = R.key(partner);
             if (i == 1) {
                 km = 1;
             } else {
@@ -127,10 +199,10 @@ __device__ inline void group_phase_a(const IterParams& P, const Rows& R, int i, 
         }
         g.f[lane] = uniform(base, kSlotForage) * P.f_mult;
         count = (int)ceil((double)((long long)dim * i) / (double)ps);
-        const int skm = R.slot(km), skp = R.slot(kp);
+        const int skm = R.key(km), skp = R.key(kp);
         sl[2] = skm;
         sl[3] = skp;
-        g.w[lane] = rank_weight(R.fit_at(skm), R.fit_at(skp), P.eps);
+        g.w[lane] = rank_weight(R.fit_at(R.slot_of(skm)), R.fit_at(R.slot_of(skp)), P.eps);
     }
     g.op[lane] = op;
     // mask: sequential partial Fisher-Yates on this lane's permutation
@@ -182,8 +254,8 @@ __device__ inline void group_extra_pairs(const IterParams& P, const Rows& R, int
             kp = i + (k + 1);
             if (kp > ps) kp = ps;
         }
-        g.ws.pk[2 * k] = R.slot(km);
-        g.ws.pk[2 * k + 1] = R.slot(kp);
+        g.ws.pk[2 * k] = R.key(km);
+        g.ws.pk[2 * k + 1] = R.key(kp);
         g.ws.pw[k] = rank_weight(R.fitness(km), R.fitness(kp), P.eps);
     }
     __syncwarp();
@@ -223,14 +295,15 @@ __device__ __forceinline__ double extra_pairs_acc(const IterParams& P, const Row
                 kp = i + (k + 1);
                 if (kp > ps) kp = ps;
             }
-            skm = R.slot(km);
-            skp = R.slot(kp);
-            w = rank_weight(R.fit_at(skm), R.fit_at(skp), P.eps);
+            skm = R.key(km);
+            skp = R.key(kp);
+            w = rank_weight(R.fit_at(R.slot_of(skm)), R.fit_at(R.slot_of(skp)), P.eps);
         }
-        acc = acc + w * (R.at(skm)[d] - R.at(skp)[d]);
+        acc = acc + w * (R.at_key(skm)[d] - R.at_key(skp)[d]);
     }
     return acc;
 }
+
 
 __device__ __forceinline__ double clampv(double c, double lo, double hi) {
     if (c < lo) c = lo;
@@ -238,142 +311,204 @@ __device__ __forceinline__ double clampv(double c, double lo, double hi) {
     return c;
 }
 
-// Phase B for member p (rank i) of the group: warp-cooperative.
-// MAXC > 0: rows held in registers (dim <= 32*MAXC).  MAXC == 0: streaming.
-template <int MAXC, class Rows>
-__device__ inline UpdateResult group_phase_b(const IterParams& P, const ObjDesc& O, const Rows& R, int i, int p,
-                                             double* out_rows, int out_ld, bool out_by_slot, const GroupScratch& g,
-                                             int lane) {
+__device__ __forceinline__ bool two_term_arrays(int code) { return code == OBJ_HGBAT || code == OBJ_GRIEWANK; }
+
+// Per-dimension fitness terms of candidate value c at dimension d (c_prev =
+// candidate value at d-1, valid when d >= 1).  Row T1 (and T2 for the
+// two-array objectives) belongs to one protozoon.  Each term is rounded
+// exactly as the reference's accumulation loop rounds it
+// (numba_backend.py:96-131).
+__device__ __forceinline__ void write_terms(const ObjDesc& O, double* T1, double* T2, int d, double c, double c_prev) {
+    switch (O.code) {
+    case OBJ_SPHERE:
+    case OBJ_BENT_CIGAR:
+        T1[d] = c * c;
+        break;
+    case OBJ_ELLIPTIC:
+        T1[d] = (O.table[d] * c) * c;
+        break;
+    case OBJ_HGBAT:
+        T1[d] = c;
+        T2[d] = c * c;
+        break;
+    case OBJ_ROSENBROCK:
+        if (d >= 1) {
+            const double a = c - c_prev * c_prev;
+            const double b = c_prev - 1.0;
+            T1[d - 1] = 100.0 * (a * a) + b * b;
+        }
+        break;
+    case OBJ_GRIEWANK:
+        T1[d] = c * c;
+        T2[d] = cos(c / sqrt((double)d + 1.0));
+        break;
+    default:
+        if (d == 0) {
+            long long idx = (long long)floor(c + 0.5);
+            if (idx < 0) idx = 0;
+            if (idx > O.table_len - 1) idx = O.table_len - 1;
+            T1[0] = O.table[idx];
+        }
+        break;
+    }
+}
+
+// Sequential left-to-right fold of one protozoon's terms (one lane).
+__device__ inline double fold_terms(const ObjDesc& O, const double* T1, const double* T2, int dim) {
+    double s = 0.0;
+    switch (O.code) {
+    case OBJ_SPHERE:
+    case OBJ_ELLIPTIC:
+#pragma unroll 4
+        for (int d = 0; d < dim; d++) s += T1[d];
+        return s;
+    case OBJ_BENT_CIGAR:
+#pragma unroll 4
+        for (int d = 1; d < dim; d++) s += T1[d];
+        return T1[0] + 1e6 * s;
+    case OBJ_HGBAT: {
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll 4
+        for (int d = 0; d < dim; d++) {
+            s1 += T1[d];
+            s2 += T2[d];
+        }
+        return sqrt(fabs(s2 * s2 - s1 * s1)) + (0.5 * s2 + s1) / (double)dim + 0.5;
+    }
+    case OBJ_ROSENBROCK:
+#pragma unroll 4
+        for (int d = 0; d < dim - 1; d++) s += T1[d];
+        return s;
+    case OBJ_GRIEWANK: {
+        double p = 1.0;
+#pragma unroll 4
+        for (int d = 0; d < dim; d++) {
+            s += T1[d];
+            p *= T2[d];
+        }
+        return 1.0 + s / 4000.0 - p;
+    }
+    default:
+        return T1[0];
+    }
+}
+
+enum OutMode : int {
+    OUT_SEL = 0,    // speculative write to the slot's alternate buffer, flip sel_next on accept
+    OUT_FIXUP = 1,  // write the candidate to the output row; rewrite rejected rows with the old row
+};
+
+// Candidate of member p (rank i) of the group, warp-cooperative: computes
+// the clamped candidate, writes it to `cand_out`, stores its fitness terms in
+// rows (T1, T2) and returns the finiteness vote.
+template <int MAXC, bool MANY, class Rows>
+__device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, const Rows& R, int i, int p,
+                                       double* cand_out, double* T1, double* T2, const GroupScratch& g, int lane) {
     const int dim = P.dim;
     const int op = g.op[p];
     const int* sl = g.slot + 4 * p;
-    const int own = sl[0];
-    const double* x = R.at(own);
-    const double fit_i = R.fit_at(own);
+    const double* x = R.at_key(sl[0]);
     const double f = g.f[p];
-    const double w0 = g.w[p];
-    const double sgn = g.sgn[p];
-    const bool many = P.npairs > 1 && (op == OP_AUTOTROPH || op == OP_HETEROTROPH);
+    const bool many = MANY && op >= OP_AUTOTROPH;
     uint64_t base = 0;
     if (op != OP_AUTOTROPH || many) base = stream_base(P.seed, P.key_iteration, (uint64_t)i);
     if (many) group_extra_pairs(P, R, i, op, base, g, lane);
-    const double* xj = (op == OP_AUTOTROPH) ? R.at(sl[1]) : x;
-    const double* xm = (op >= OP_AUTOTROPH) ? R.at(sl[2]) : x;
-    const double* xp = (op >= OP_AUTOTROPH) ? R.at(sl[3]) : x;
-    const double inv_np = (double)P.npairs;
-    double* out_row = out_rows + (size_t)(out_by_slot ? own : i - 1) * out_ld;
+    const double* xj = R.at_key(sl[op == OP_AUTOTROPH ? 1 : 0]);
+    const double* xm = R.at_key(sl[op >= OP_AUTOTROPH ? 2 : 0]);
+    const double* xp = R.at_key(sl[op >= OP_AUTOTROPH ? 3 : 0]);
+    const double w0 = g.w[p];
+    const double sgn = g.sgn[p];
+    const double npd = (double)P.npairs;
+    const unsigned* mb = g.bits + p * g.words;
+    bool ok = true;
+    double carry = 0.0;  // candidate at d-1 for lane 0 of the next chunk
 
-    auto cand_at = [&](int d, double xd, double aj, double am, double ap) -> double {
-        double c;
-        if (op == OP_DORMANCY) {
-            c = P.lower + uniform(base, kVectorBase + (uint64_t)d) * P.span;
-        } else if (op == OP_REPRODUCTION) {
-            const double off = P.lower + uniform(base, kVectorBase + (uint64_t)d) * P.span;
-            c = xd + (f * off) * gmask(g, p, d);
-        } else {
-            double acc = 0.0;
-            acc = acc + w0 * (am - ap);
+    auto mk = [&](int d) -> double { return ((mb[d >> 5] >> (d & 31)) & 1u) ? 1.0 : 0.0; };
+    auto forage = [&](int d, double xd, double aj, double am, double ap) -> double {
+        double acc = 0.0;
+        acc = acc + w0 * (am - ap);
+        double ep = acc;
+        if constexpr (MANY) {
             if (many) acc = extra_pairs_acc(P, R, i, op, base, g, acc, d);
-            const double ep = P.npairs == 1 ? acc : acc / inv_np;
-            double direction;
-            if (op == OP_AUTOTROPH) {
-                direction = (aj - xd) + ep;
-            } else {
-                const double uv = uniform(base, kVectorBase + (uint64_t)d);
-                direction = ((1.0 + (sgn * uv) * P.decay) * xd - xd) + ep;
-            }
-            c = xd + (f * direction) * gmask(g, p, d);
+            ep = acc / npd;
         }
-        return clampv(c, P.lower, P.upper);
+        double direction;
+        if (op == OP_AUTOTROPH) {
+            direction = (aj - xd) + ep;
+        } else {
+            const double uv = uniform(base, kVectorBase + (uint64_t)d);
+            direction = ((1.0 + (sgn * uv) * P.decay) * xd - xd) + ep;
+        }
+        return xd + (f * direction) * mk(d);
+    };
+    // every lane calls finish() once per chunk (the shuffles need the full warp)
+    auto finish = [&](int d, double c, bool valid) {
+        c = clampv(c, P.lower, P.upper);
+        double prev = __shfl_up_sync(kFull, c, 1);
+        if (lane == 0) prev = carry;
+        carry = __shfl_sync(kFull, c, 31);
+        if (valid) {
+            ok = ok && isfinite(c);
+            cand_out[d] = c;
+            write_terms(O, T1, T2, d, c, prev);
+        }
     };
 
-    UpdateResult res;
-    res.accepted = false;
-    res.warned = false;
-    res.fitness = fit_i;
-    bool ok = true;
-    if constexpr (MAXC > 0) {
-        double xv[MAXC], aj[MAXC], am[MAXC], ap[MAXC], cv[MAXC];
+    if (MAXC > 0 && op == OP_AUTOTROPH) {
+        // row loads issued LC chunks at a time (4 rows x LC chunks in flight)
+        constexpr int LC = (APO_LOAD_CHUNKS < MAXC ? APO_LOAD_CHUNKS : (MAXC > 0 ? MAXC : 1));
 #pragma unroll
-        for (int c = 0; c < MAXC; c++) {
-            const int d = lane + 32 * c;
-            if (d < dim) {
-                xv[c] = x[d];
-                if (op == OP_AUTOTROPH) aj[c] = xj[d];
-                if (op >= OP_AUTOTROPH) {
-                    am[c] = xm[d];
-                    ap[c] = xp[d];
+        for (int c0 = 0; c0 < (MAXC > 0 ? MAXC : 1); c0 += LC) {
+            double xv[LC], aj[LC], am[LC], ap[LC];
+#pragma unroll
+            for (int u = 0; u < LC; u++) {
+                const int d = lane + 32 * (c0 + u);
+                if (d < dim) {
+                    xv[u] = x[d];
+                    aj[u] = xj[d];
+                    am[u] = xm[d];
+                    ap[u] = xp[d];
                 }
             }
-        }
 #pragma unroll
-        for (int c = 0; c < MAXC; c++) {
-            const int d = lane + 32 * c;
-            if (d < dim) {
-                cv[c] = cand_at(d, xv[c], aj[c], am[c], ap[c]);
-                ok = ok && isfinite(cv[c]);
-                g.ws.cand[d] = cv[c];
-            }
-        }
-        ok = __all_sync(kFull, ok);
-        __syncwarp();
-        if (ok) {
-            const double nf = eval_warp(O, g.ws.cand, g.ws.terms, dim, lane);
-            if (isfinite(nf)) {
-                res.accepted = nf < fit_i;
-                if (res.accepted) res.fitness = nf;
-            } else {
-                res.warned = true;
-            }
-        } else {
-            res.warned = true;
-        }
-        if (res.accepted || out_row != x) {
-#pragma unroll
-            for (int c = 0; c < MAXC; c++) {
+            for (int u = 0; u < LC; u++) {
+                const int c = c0 + u;
                 const int d = lane + 32 * c;
-                if (d < dim) out_row[d] = res.accepted ? cv[c] : xv[c];
+                if (32 * c < dim) finish(d, d < dim ? forage(d, xv[u], aj[u], am[u], ap[u]) : 0.0, d < dim);
             }
         }
     } else {
-        for (int d = lane; d < dim; d += 32) {
-            const double xd = x[d];
-            const double c = cand_at(d, xd, op == OP_AUTOTROPH ? xj[d] : 0.0, op >= OP_AUTOTROPH ? xm[d] : 0.0,
-                                     op >= OP_AUTOTROPH ? xp[d] : 0.0);
-            ok = ok && isfinite(c);
-            g.ws.cand[d] = c;
-        }
-        ok = __all_sync(kFull, ok);
-        __syncwarp();
-        if (ok) {
-            const double nf = eval_warp(O, g.ws.cand, g.ws.terms, dim, lane);
-            if (isfinite(nf)) {
-                res.accepted = nf < fit_i;
-                if (res.accepted) res.fitness = nf;
-            } else {
-                res.warned = true;
+        const int nch = (dim + 31) / 32;
+        for (int c = 0; c < nch; c++) {
+            const int d = lane + 32 * c;
+            double cv = 0.0;
+            if (d < dim) {
+                const double xd = x[d];
+                if (op == OP_DORMANCY) {
+                    cv = P.lower + uniform(base, kVectorBase + (uint64_t)d) * P.span;
+                } else if (op == OP_REPRODUCTION) {
+                    const double off = P.lower + uniform(base, kVectorBase + (uint64_t)d) * P.span;
+                    cv = xd + (f * off) * mk(d);
+                } else {
+                    cv = forage(d, xd, op == OP_AUTOTROPH ? xj[d] : 0.0, xm[d], xp[d]);
+                }
             }
-        } else {
-            res.warned = true;
-        }
-        if (res.accepted) {
-            for (int d = lane; d < dim; d += 32) out_row[d] = g.ws.cand[d];
-        } else if (out_row != x) {
-            for (int d = lane; d < dim; d += 32) out_row[d] = x[d];
+            finish(d, cv, d < dim);
         }
     }
-    __syncwarp();
-    return res;
+    return __all_sync(kFull, ok);
 }
 
-// One group of up to 32 ranks [i0, i0+n) on one warp.  in_dr via bits or
-// bytes; results: fitness written to out_fit (by slot or rank), optional
-// acc/warn bytes by rank; returns (min sort key, warned count) via refs.
-template <int MAXC, class Rows>
+// One group of n <= 32 consecutive ranks [i0, i0+n) on one warp.
+// MODE OUT_SEL:   rows via SelSlots; candidates go to R.alt(slot); sel_next and
+//                 out_fit (by slot) record the kept state.
+// MODE OUT_FIXUP: candidates go to out_rows (by slot if out_by_slot, else by
+//                 rank); rejected rows are then rewritten with the old row.
+template <int MAXC, int MODE, class Rows>
 __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const Rows& R, int i0, int n,
                                     const uint8_t* in_dr_bytes, const unsigned* in_dr_bits, const double* p_dr,
                                     double* out_rows, double* out_fit, bool out_by_slot, uint8_t* out_acc,
-                                    uint8_t* out_warn, const GroupScratch& g, int lane,
+                                    uint8_t* out_warn, uint8_t* sel_next, const GroupScratch& g, int lane,
                                     unsigned long long& my_min, unsigned& my_warn) {
     if (lane < n) {
         const int r0 = i0 - 1 + lane;
@@ -381,20 +516,69 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
         group_phase_a(P, R, i0 + lane, dr, dr ? p_dr[r0] : 0.0, g, lane);
     }
     __syncwarp();
-    for (int p = 0; p < n; p++) {
-        const int i = i0 + p;
-        const UpdateResult res =
-            group_phase_b<MAXC>(P, O, R, i, p, out_rows, P.ld, out_by_slot, g, lane);
-        if (lane == 0) {
-            out_fit[out_by_slot ? g.slot[4 * p] : i - 1] = res.fitness;
-            if (out_acc) out_acc[i - 1] = res.accepted ? 1 : 0;
-            if (out_warn) out_warn[i - 1] = res.warned ? 1 : 0;
-            const unsigned long long k = sort_key(res.fitness);
-            my_min = k < my_min ? k : my_min;
-            my_warn += res.warned ? 1u : 0u;
+    const bool two = two_term_arrays(O.code);
+    const int B = two ? g.batch / 2 : g.batch;
+    double* T2base = g.T + (size_t)(g.batch / 2) * g.tstride;
+    for (int h = 0; h < n; h += B) {
+        const int nb = min(B, n - h);
+        unsigned okmask = 0;
+        for (int q = 0; q < nb; q++) {
+            const int p = h + q, i = i0 + p;
+            const int own_key = g.slot[4 * p];
+            double* dst;
+            if constexpr (MODE == OUT_SEL) dst = R.alt_key(own_key);
+            else dst = out_rows + (size_t)(out_by_slot ? R.slot_of(own_key) : i - 1) * P.ld;
+            double* T1 = g.T + (size_t)q * g.tstride;
+            double* T2 = two ? T2base + (size_t)q * g.tstride : nullptr;
+            const bool ok = P.npairs > 1 ? group_candidate<MAXC, true>(P, O, R, i, p, dst, T1, T2, g, lane)
+                                          : group_candidate<MAXC, false>(P, O, R, i, p, dst, T1, T2, g, lane);
+            okmask |= (ok ? 1u : 0u) << q;
         }
+        __syncwarp();
+        bool acc = false, warned = false;
+        if (lane < nb) {
+            const int p = h + lane, i = i0 + p;
+            const int own_key = g.slot[4 * p];
+            const int own = R.slot_of(own_key);
+            const double fit_i = R.fit_at(own);
+            double kept = fit_i;
+            if ((okmask >> lane) & 1u) {
+                const double nf = fold_terms(O, g.T + (size_t)lane * g.tstride,
+                                             two ? T2base + (size_t)lane * g.tstride : nullptr, P.dim);
+                if (isfinite(nf)) {
+                    acc = nf < fit_i;
+                    if (acc) kept = nf;
+                } else {
+                    warned = true;
+                }
+            } else {
+                warned = true;
+            }
+            out_fit[out_by_slot ? own : i - 1] = kept;
+            if (out_acc) out_acc[i - 1] = acc ? 1 : 0;
+            if (out_warn) out_warn[i - 1] = warned ? 1 : 0;
+            if constexpr (MODE == OUT_SEL) {
+                const uint8_t cur = (uint8_t)(own_key & 1);
+                sel_next[own] = acc ? (uint8_t)(cur ^ 1) : cur;
+            }
+            const unsigned long long k = sort_key(kept);
+            my_min = k < my_min ? k : my_min;
+            my_warn += warned ? 1u : 0u;
+        }
+        if constexpr (MODE == OUT_FIXUP) {
+            unsigned rej = __ballot_sync(kFull, lane < nb && !acc);
+            while (rej) {
+                const int q = __ffs(rej) - 1;
+                rej &= rej - 1;
+                const int p = h + q, i = i0 + p;
+                const int own_key = g.slot[4 * p];
+                const double* x = R.at_key(own_key);
+                double* dst = out_rows + (size_t)(out_by_slot ? R.slot_of(own_key) : i - 1) * P.ld;
+                for (int d = lane; d < P.dim; d += 32) dst[d] = x[d];
+            }
+        }
+        __syncwarp();
     }
-    __syncwarp();
 }
 
 }  // namespace apo

@@ -105,44 +105,41 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
 }
 
 // ---------------------------------------------------------------------------
-template <bool INDIRECT>
-__global__ void __launch_bounds__(kThreads) k_update(IterParams P, ObjDesc O, const double* __restrict__ pos,
-                                                     const double* __restrict__ fit, const int* __restrict__ order,
-                                                     const uint8_t* __restrict__ in_dr_bytes,
-                                                     const unsigned* __restrict__ in_dr_bits,
-                                                     const double* __restrict__ p_dr, double* __restrict__ out_pos,
-                                                     double* __restrict__ out_fit, uint8_t* __restrict__ out_acc,
-                                                     uint8_t* __restrict__ out_warn,
-                                                     unsigned long long* __restrict__ warn_count,
-                                                     unsigned long long* __restrict__ trace_key) {
-    extern __shared__ __align__(16) unsigned char smem[];
+// Update launch arguments.  SEL mode (device-resident loop): rows live in
+// pos0/pos1 selected per slot by sel[], ranks map to slots through order[],
+// candidates go to the alternate buffer and sel_next/out_fit (by slot)
+// record what is kept.  Dense mode (run_updates boundary): rank-ordered rows
+// in pos -> out_pos, out_fit/out_acc/out_warn by rank.
+struct UpdArgs {
+    IterParams P;
+    ObjDesc O;
+    const double* pos0;
+    const double* pos1;
+    const uint8_t* sel;
+    uint8_t* sel_next;
+    const double* pos;
+    double* out_pos;
+    const double* fit;
+    const int* order;
+    double* out_fit;
+    const uint8_t* in_dr_bytes;
+    const unsigned* in_dr_bits;
+    const double* p_dr;
+    uint8_t* out_acc;
+    uint8_t* out_warn;
+    unsigned long long* warn_count;
+    unsigned long long* trace_key;
+};
+
+__device__ __forceinline__ void block_finish(unsigned long long my_min, unsigned my_warn,
+                                             unsigned long long* warn_count, unsigned long long* trace_key) {
     __shared__ unsigned long long red_min[32];
     __shared__ unsigned red_warn[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const WarpScratch s = warp_scratch(smem + (size_t)warp * warp_scratch_bytes(P.dim), P.dim);
-    unsigned long long my_min = ~0ull;
-    unsigned my_warn = 0;
-    for (int r0 = blockIdx.x * nwarps + warp; r0 < P.ps; r0 += gridDim.x * nwarps) {
-        const bool dr = in_dr_bits ? ((in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0 : in_dr_bytes[r0] != 0;
-        const double pdr = dr ? p_dr[r0] : 0.0;
-        UpdateResult res;
-        if (INDIRECT) {
-            const OrderedRows R{pos, fit, order, P.ld};
-            const int slot = order[r0];
-            res = update_protozoon(P, O, R, r0 + 1, dr, pdr, out_pos + (size_t)slot * P.ld, s, lane);
-            if (lane == 0) out_fit[slot] = res.fitness;
-        } else {
-            const DenseRows R{pos, fit, P.ld};
-            res = update_protozoon(P, O, R, r0 + 1, dr, pdr, out_pos + (size_t)r0 * P.ld, s, lane);
-            if (lane == 0) {
-                out_fit[r0] = res.fitness;
-                if (out_acc) out_acc[r0] = res.accepted ? 1 : 0;
-                if (out_warn) out_warn[r0] = res.warned ? 1 : 0;
-            }
-        }
-        const unsigned long long k = sort_key(res.fitness);
-        my_min = k < my_min ? k : my_min;
-        my_warn += res.warned ? 1u : 0u;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long m2 = __shfl_xor_sync(kFull, my_min, o);
+        my_min = m2 < my_min ? m2 : my_min;
+        my_warn += __shfl_xor_sync(kFull, my_warn, o);
     }
     if (lane == 0) {
         red_min[warp] = my_min;
@@ -161,17 +158,53 @@ __global__ void __launch_bounds__(kThreads) k_update(IterParams P, ObjDesc O, co
     }
 }
 
-// Group path (dim <= 256): one warp per 32 consecutive ranks, see apo_group.cuh.
-template <bool INDIRECT, int MAXC>
-__global__ void __launch_bounds__(kThreads) k_update_group(
-    IterParams P, ObjDesc O, const double* __restrict__ pos, const double* __restrict__ fit,
-    const int* __restrict__ order, const uint8_t* __restrict__ in_dr_bytes, const unsigned* __restrict__ in_dr_bits,
-    const double* __restrict__ p_dr, double* __restrict__ out_pos, double* __restrict__ out_fit,
-    uint8_t* __restrict__ out_acc, uint8_t* __restrict__ out_warn, unsigned long long* __restrict__ warn_count,
-    unsigned long long* __restrict__ trace_key) {
+// Warp-per-protozoon path (dim > 256).
+template <bool SEL>
+__global__ void __launch_bounds__(kThreads) k_update(UpdArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned long long red_min[32];
-    __shared__ unsigned red_warn[32];
+    const IterParams& P = A.P;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const WarpScratch s = warp_scratch(smem + (size_t)warp * warp_scratch_bytes(P.dim), P.dim);
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    for (int r0 = blockIdx.x * nwarps + warp; r0 < P.ps; r0 += gridDim.x * nwarps) {
+        const bool dr = A.in_dr_bits ? ((A.in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0 : A.in_dr_bytes[r0] != 0;
+        const double pdr = dr ? A.p_dr[r0] : 0.0;
+        UpdateResult res;
+        if constexpr (SEL) {
+            const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
+            const int slot = A.order[r0];
+            res = update_protozoon(P, A.O, R, r0 + 1, dr, pdr, R.alt(slot), s, lane);
+            if (lane == 0) {
+                A.out_fit[slot] = res.fitness;
+                A.sel_next[slot] = A.sel[slot] ^ 1;  // the full kept row went to the alternate buffer
+            }
+        } else {
+            const DenseRows R{A.pos, A.fit, P.ld};
+            res = update_protozoon(P, A.O, R, r0 + 1, dr, pdr, A.out_pos + (size_t)r0 * P.ld, s, lane);
+            if (lane == 0) {
+                A.out_fit[r0] = res.fitness;
+                if (A.out_acc) A.out_acc[r0] = res.accepted ? 1 : 0;
+                if (A.out_warn) A.out_warn[r0] = res.warned ? 1 : 0;
+            }
+        }
+        if (lane == 0) {
+            const unsigned long long k = sort_key(res.fitness);
+            my_min = k < my_min ? k : my_min;
+            my_warn += res.warned ? 1u : 0u;
+        }
+    }
+    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
+}
+
+// Group path (dim <= 256): one warp per 32 consecutive ranks, see apo_group.cuh.
+#ifndef APO_GROUP_MIN_BLOCKS
+#define APO_GROUP_MIN_BLOCKS 1
+#endif
+template <bool SEL, int MAXC>
+__global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group(UpdArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const IterParams& P = A.P;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const GroupScratch g = group_scratch(smem + (size_t)warp * group_scratch_bytes(P.dim), P.dim);
     unsigned long long my_min = ~0ull;
@@ -180,31 +213,18 @@ __global__ void __launch_bounds__(kThreads) k_update_group(
     for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
         const int i0 = grp * 32 + 1;
         const int n = min(32, P.ps - grp * 32);
-        if (INDIRECT) {
-            const OrderedSlots R{pos, fit, order, P.ld};
-            update_group<MAXC>(P, O, R, i0, n, in_dr_bytes, in_dr_bits, p_dr, out_pos, out_fit, true, out_acc,
-                               out_warn, g, lane, my_min, my_warn);
+        if constexpr (SEL) {
+            const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
+            update_group<MAXC, OUT_SEL>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
+                                        true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn);
         } else {
-            const DenseSlots R{pos, fit, P.ld};
-            update_group<MAXC>(P, O, R, i0, n, in_dr_bytes, in_dr_bits, p_dr, out_pos, out_fit, false, out_acc,
-                               out_warn, g, lane, my_min, my_warn);
+            const DenseSlots R{A.pos, A.fit, P.ld};
+            update_group<MAXC, OUT_FIXUP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
+                                          A.out_fit, false, A.out_acc, A.out_warn, nullptr, g, lane, my_min,
+                                          my_warn);
         }
     }
-    if (lane == 0) {
-        red_min[warp] = my_min;
-        red_warn[warp] = my_warn;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long m = ~0ull;
-        unsigned w = 0;
-        for (int k = 0; k < nwarps; k++) {
-            m = red_min[k] < m ? red_min[k] : m;
-            w += red_warn[k];
-        }
-        if (trace_key && m != ~0ull) atomicMin(trace_key, m);
-        if (warn_count && w) atomicAdd(warn_count, (unsigned long long)w);
-    }
+    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
 }
 
 __global__ void __launch_bounds__(kThreads) k_init(uint64_t seed, int ps, int dim, int ld, double lower,
@@ -310,14 +330,16 @@ __global__ void k_dr_resolve(int count, int n, uint64_t base, const unsigned lon
     }
 }
 
-__global__ void k_gather_rows(int n, int dim, int ld, const double* __restrict__ pos, const double* __restrict__ fit,
-                              const int* __restrict__ order, double* __restrict__ out_pos,
-                              double* __restrict__ out_fit) {
+__global__ void k_gather_rows(int n, int dim, int ld, const double* __restrict__ pos0,
+                              const double* __restrict__ pos1, const uint8_t* __restrict__ sel,
+                              const double* __restrict__ fit, const int* __restrict__ order,
+                              double* __restrict__ out_pos, double* __restrict__ out_fit) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (int r = warp; r < n; r += nw) {
         const int slot = order[r];
-        for (int d = lane; d < dim; d += 32) out_pos[(size_t)r * dim + d] = pos[(size_t)slot * ld + d];
+        const double* src = (sel[slot] ? pos1 : pos0) + (size_t)slot * ld;
+        for (int d = lane; d < dim; d += 32) out_pos[(size_t)r * dim + d] = src[d];
         if (lane == 0 && out_fit) out_fit[r] = fit[slot];
     }
 }
@@ -433,16 +455,17 @@ __global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
     const ObjDesc O = A.objs[run];
     double* trace = A.trace ? A.trace + (size_t)run * (A.n_iters + 1) : nullptr;
 
-    // initialisation (engine.py:116-139)
+    // initialisation (engine.py:116-139); the init scratch aliases this warp's group scratch
     unsigned long long my_min = ~0ull;
+    const WarpScratch iws = warp_scratch(wbase, dim);
     for (int r0 = warp; r0 < ps; r0 += nwarps) {
         const uint64_t base = stream_base(seed, 0, (uint64_t)(r0 + 1));
         double* row = pos[0] + (size_t)r0 * ld;
         for (int d = lane; d < dim; d += 32) row[d] = A.lower + uniform(base, (uint64_t)d) * A.span;
         __syncwarp();
-        for (int d = lane; d < dim; d += 32) ws.cand[d] = row[d];
+        for (int d = lane; d < dim; d += 32) iws.cand[d] = row[d];
         __syncwarp();
-        const double f = eval_warp(O, ws.cand, ws.terms, dim, lane);
+        const double f = eval_warp(O, iws.cand, iws.terms, dim, lane);
         if (lane == 0) {
             fit[0][r0] = f;
             keys[r0] = sort_key(f);
@@ -509,8 +532,8 @@ __global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
             const int G = min(32, (ps + nwarps - 1) / nwarps);
             for (int q = warp; q * G < ps; q += nwarps) {
                 const int i0 = q * G + 1;
-                update_group<MAXC>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr, pos[nxt], fit[nxt],
-                                   true, nullptr, nullptr, g, lane, my_min, my_warn);
+                update_group<MAXC, OUT_FIXUP>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr, pos[nxt],
+                                              fit[nxt], true, nullptr, nullptr, nullptr, g, lane, my_min, my_warn);
             }
             __syncthreads();
             for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) keys[sl] = sort_key(fit[nxt][sl]);
@@ -529,6 +552,11 @@ __global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
                     my_warn += res.warned ? 1u : 0u;
                 }
             }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long m2 = __shfl_xor_sync(kFull, my_min, o);
+            my_min = m2 < my_min ? m2 : my_min;
+            my_warn += __shfl_xor_sync(kFull, my_warn, o);
         }
         if (lane == 0) {
             red_min[warp] = my_min;
@@ -568,47 +596,32 @@ __global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
         for (int r = threadIdx.x; r < ps; r += blockDim.x) A.final_fit[(size_t)run * ps + r] = fit[cur][order[r]];
 }
 
-int launch_update(bool indirect, const IterParams& P, const ObjDesc& O, const double* pos, const double* fit,
-                  const int* order, const uint8_t* in_dr_bytes, const unsigned* in_dr_bits, const double* p_dr,
-                  double* out_pos, double* out_fit, uint8_t* out_acc, uint8_t* out_warn,
-                  unsigned long long* warn_count, unsigned long long* trace_key, cudaStream_t st) {
-    if (P.dim <= kGroupMaxDim) {
-        const size_t smem = group_scratch_bytes(P.dim) * (size_t)kWarps;
-        const void* fn;
-        if (P.dim <= 32) fn = indirect ? (const void*)k_update_group<true, 1> : (const void*)k_update_group<false, 1>;
-        else if (P.dim <= 64) fn = indirect ? (const void*)k_update_group<true, 2> : (const void*)k_update_group<false, 2>;
-        else if (P.dim <= 128) fn = indirect ? (const void*)k_update_group<true, 4> : (const void*)k_update_group<false, 4>;
-        else fn = indirect ? (const void*)k_update_group<true, 0> : (const void*)k_update_group<false, 0>;
-        if (int rc = set_smem(fn, smem)) return rc;
-        int per_sm = 1;
-        APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
-        if (per_sm < 1) per_sm = 1;
-        const long long need = ((long long)(P.ps + 31) / 32 + kWarps - 1) / kWarps;
-        const long long cap = (long long)per_sm * num_sms();
-        const int grid = (int)(need < cap ? need : cap);
-        void* args[] = {(void*)&P,        (void*)&O,     (void*)&pos,     (void*)&fit,      (void*)&order,
-                        (void*)&in_dr_bytes, (void*)&in_dr_bits, (void*)&p_dr, (void*)&out_pos, (void*)&out_fit,
-                        (void*)&out_acc,  (void*)&out_warn, (void*)&warn_count, (void*)&trace_key};
-        APO_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, st));
-        return APO_OK;
-    }
-    const int w = warps_for_dim(P.dim);
-    const size_t smem = warp_scratch_bytes(P.dim) * (size_t)w;
-    const void* fn = indirect ? (const void*)k_update<true> : (const void*)k_update<false>;
+template <bool SEL>
+const void* pick_update_kernel(int dim) {
+    if (dim <= 32) return (const void*)k_update_group<SEL, 1>;
+    if (dim <= 64) return (const void*)k_update_group<SEL, 2>;
+    if (dim <= 128) return (const void*)k_update_group<SEL, 4>;
+    if (dim <= kGroupMaxDim) return (const void*)k_update_group<SEL, 0>;
+    return (const void*)k_update<SEL>;
+}
+
+int launch_update(bool sel_mode, const UpdArgs& A, cudaStream_t st) {
+    const int dim = A.P.dim;
+    const bool group = dim <= kGroupMaxDim;
+    const int w = group ? kWarps : warps_for_dim(dim);
+    const size_t smem = (group ? group_scratch_bytes(dim) : warp_scratch_bytes(dim)) * (size_t)w;
+    const void* fn = sel_mode ? pick_update_kernel<true>(dim) : pick_update_kernel<false>(dim);
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
     if (per_sm < 1) per_sm = 1;
-    const long long need = ((long long)P.ps + w - 1) / w;
+    const long long units = group ? ((long long)A.P.ps + 31) / 32 : (long long)A.P.ps;
+    const long long need = (units + w - 1) / w;
     const long long cap = (long long)per_sm * num_sms();
     const int grid = (int)(need < cap ? need : cap);
-    if (indirect)
-        k_update<true><<<grid, 32 * w, smem, st>>>(P, O, pos, fit, order, in_dr_bytes, in_dr_bits, p_dr, out_pos,
-                                                   out_fit, out_acc, out_warn, warn_count, trace_key);
-    else
-        k_update<false><<<grid, 32 * w, smem, st>>>(P, O, pos, fit, order, in_dr_bytes, in_dr_bits, p_dr, out_pos,
-                                                    out_fit, out_acc, out_warn, warn_count, trace_key);
-    APO_CUDA(cudaGetLastError());
+    UpdArgs a = A;
+    void* args[] = {(void*)&a};
+    APO_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(32 * w), args, smem, st));
     return APO_OK;
 }
 
@@ -669,7 +682,8 @@ struct apo_run {
     double pf_max, lower, upper, eps;
     ObjDesc obj;
     cudaStream_t stream;
-    double* pos[2];
+    double* pos[2];  // two row buffers; sel[cur][slot] picks the current one
+    uint8_t* sel[2];
     double* fit[2];
     int cur;
     int* order;
@@ -731,8 +745,19 @@ int apo_run_updates_obj(const double* positions, const double* fitness, const ui
     P.f_mult = f_mult;
     P.decay = decay;
     if (warn_count) APO_CUDA(cudaMemsetAsync(warn_count, 0, sizeof(unsigned long long), as_stream(stream)));
-    return launch_update(false, P, to_desc(objective_host), positions, fitness, nullptr, in_dr, nullptr, p_dr,
-                         out_pos, out_fit, out_acc, out_warn, warn_count, nullptr, as_stream(stream));
+    UpdArgs A{};
+    A.P = P;
+    A.O = to_desc(objective_host);
+    A.pos = positions;
+    A.out_pos = out_pos;
+    A.fit = fitness;
+    A.out_fit = out_fit;
+    A.in_dr_bytes = in_dr;
+    A.p_dr = p_dr;
+    A.out_acc = out_acc;
+    A.out_warn = out_warn;
+    A.warn_count = warn_count;
+    return launch_update(false, A, as_stream(stream));
 }
 
 int apo_run_updates(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
@@ -894,6 +919,8 @@ int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iteration
     };
     alloc((void**)&r->pos[0], rows);
     alloc((void**)&r->pos[1], rows);
+    alloc((void**)&r->sel[0], (size_t)ps);
+    alloc((void**)&r->sel[1], (size_t)ps);
     alloc((void**)&r->fit[0], 8 * (size_t)ps);
     alloc((void**)&r->fit[1], 8 * (size_t)ps);
     alloc((void**)&r->order, 4 * (size_t)ps);
@@ -936,6 +963,7 @@ int apo_run_initialize(apo_run* r) {
     APO_CUDA(cudaGetLastError());
     k_iota<<<grid_for(r->ps, 256), 256, 0, st>>>((int)r->ps, r->order);
     APO_CUDA(cudaGetLastError());
+    APO_CUDA(cudaMemsetAsync(r->sel[0], 0, (size_t)r->ps, st));
     r->cur = 0;
     r->iters = 0;
     r->initialized = true;
@@ -984,10 +1012,21 @@ int apo_run_iterate(apo_run* r, int64_t n) {
             }
             APO_CUDA(cudaEventRecord(ev[0], st));
         }
-        if (int rc = launch_update(true, P, r->obj, r->pos[r->cur], r->fit[r->cur], r->order, nullptr, r->dr_bits,
-                                   r->p_dr, r->pos[r->cur ^ 1], r->fit[r->cur ^ 1], nullptr, nullptr, r->warn,
-                                   r->trace_keys + t + 1, st))
-            return rc;
+        UpdArgs A{};
+        A.P = P;
+        A.O = r->obj;
+        A.pos0 = r->pos[0];
+        A.pos1 = r->pos[1];
+        A.sel = r->sel[r->cur];
+        A.sel_next = r->sel[r->cur ^ 1];
+        A.fit = r->fit[r->cur];
+        A.out_fit = r->fit[r->cur ^ 1];
+        A.order = r->order;
+        A.in_dr_bits = r->dr_bits;
+        A.p_dr = r->p_dr;
+        A.warn_count = r->warn;
+        A.trace_key = r->trace_keys + t + 1;
+        if (int rc = launch_update(true, A, st)) return rc;
         if (r->profile) APO_CUDA(cudaEventRecord(ev[1], st));
         r->cur ^= 1;
         r->iters++;
@@ -1013,8 +1052,9 @@ int apo_run_population(apo_run* r, double* positions, double* fitness, int is_ho
         APO_CUDA(cudaMallocAsync((void**)&dpos, 8 * (size_t)r->ps * r->dim, st));
         APO_CUDA(cudaMallocAsync((void**)&dfit, 8 * (size_t)r->ps, st));
     }
-    k_gather_rows<<<grid_for(r->ps * 32, 256), 256, 0, st>>>((int)r->ps, (int)r->dim, (int)r->ld, r->pos[r->cur],
-                                                             r->fit[r->cur], r->order, dpos, dfit);
+    k_gather_rows<<<grid_for(r->ps * 32, 256), 256, 0, st>>>((int)r->ps, (int)r->dim, (int)r->ld, r->pos[0],
+                                                             r->pos[1], r->sel[r->cur], r->fit[r->cur], r->order,
+                                                             dpos, dfit);
     APO_CUDA(cudaGetLastError());
     if (is_host) {
         if (positions)
@@ -1042,7 +1082,10 @@ int apo_run_best(apo_run* r, double* best_fitness_host, double* best_position_ho
     if (best_fitness_host) *best_fitness_host = fit[(size_t)slot];
     if (best_row_host) *best_row_host = best;
     if (best_position_host) {
-        APO_CUDA(cudaMemcpyAsync(best_position_host, r->pos[r->cur] + (size_t)slot * r->ld, 8 * (size_t)r->dim,
+        uint8_t which = 0;
+        APO_CUDA(cudaMemcpyAsync(&which, r->sel[r->cur] + slot, 1, cudaMemcpyDeviceToHost, st));
+        APO_CUDA(cudaStreamSynchronize(st));
+        APO_CUDA(cudaMemcpyAsync(best_position_host, r->pos[which] + (size_t)slot * r->ld, 8 * (size_t)r->dim,
                                  cudaMemcpyDeviceToHost, st));
         APO_CUDA(cudaStreamSynchronize(st));
     }
@@ -1090,7 +1133,7 @@ int apo_run_profile_read(apo_run* r, double* update_ms_host, int64_t* launches_h
 int apo_run_destroy(apo_run* r) {
     if (!r) return APO_OK;
     clear_profile(r);
-    void* bufs[] = {r->pos[0], r->pos[1], r->fit[0], r->fit[1], r->order, r->keys_in, r->keys_out, r->vals_in,
+    void* bufs[] = {r->pos[0], r->pos[1], r->sel[0], r->sel[1], r->fit[0], r->fit[1], r->order, r->keys_in, r->keys_out, r->vals_in,
                     r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn};
     for (void* b : bufs)
         if (b) cudaFree(b);
