@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) k_update(UpdArgs A) {
 
 // Group path (dim <= 256): one warp per 32 consecutive ranks, see apo_group.cuh.
 #ifndef APO_GROUP_MIN_BLOCKS
-#define APO_GROUP_MIN_BLOCKS 1
+#define APO_GROUP_MIN_BLOCKS 2
 #endif
 template <bool SEL, int MAXC>
 __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group(UpdArgs A) {
