@@ -18,16 +18,58 @@ namespace apo {
 
 constexpr int kGroupMaxDim = 256;  // uint8 permutations
 
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) + mbarrier completion.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "APO_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra APO_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Row staging ring: kStages protozoa x 4 rows, per warp (HBM-resident paths).
+constexpr int kStages = 2;
+#ifndef APO_STAGE_MAX_DIM
+#define APO_STAGE_MAX_DIM 128
+#endif
+
+
 // Terms batch: protozoa whose per-dimension fitness terms are staged in shared
 // memory before 1 lane each folds them sequentially.
 #ifndef APO_LOAD_CHUNKS
-#define APO_LOAD_CHUNKS 4
+#define APO_LOAD_CHUNKS 2
 #endif
 #ifndef APO_GROUP_BATCH_SMALL_D
 #define APO_GROUP_BATCH_SMALL_D 16
 #endif
 #ifndef APO_GROUP_BATCH_LARGE_D
-#define APO_GROUP_BATCH_LARGE_D 8
+#define APO_GROUP_BATCH_LARGE_D 4
 #endif
 __host__ __device__ inline int group_batch(int dim) {
     return dim <= 64 ? APO_GROUP_BATCH_SMALL_D : APO_GROUP_BATCH_LARGE_D;
@@ -44,9 +86,16 @@ struct GroupScratch {
     int* slot;            // [32][4] own, partner, km, kp slots
     int* op;              // [32]
     double* T;            // [batch][tstride] fitness terms
+    double* ring;         // [kStages][4][rld] staged rows (nullptr if not staging)
+    uint64_t* bar;        // [kStages] mbarriers of the ring
     WarpScratch ws;       // only ws.pk / ws.pw (pair cache for npairs > 1) are used
-    int dp, words, tstride, batch;
+    int dp, words, tstride, batch, rld;
 };
+
+__host__ __device__ inline int ring_ld(int dim) { return (dim + 1) & ~1; }
+__host__ __device__ inline size_t ring_bytes(int dim, bool stage) {
+    return stage ? (size_t)kStages * 4 * 8 * (size_t)ring_ld(dim) + 16 * kStages : 0;
+}
 
 // Layout: [header: scalars, slots, ops, pair cache, mask bits][union: phase-A
 // permutations (32 x dp bytes) | phase-B terms (batch x tstride doubles)].
@@ -58,13 +107,17 @@ __host__ __device__ inline size_t group_head_bytes(int dim) {
     return (b + 15) & ~(size_t)15;
 }
 
-__host__ __device__ inline size_t group_scratch_bytes(int dim) {
+__host__ __device__ inline size_t group_union_bytes(int dim) {
     const size_t perm = 32 * (size_t)((dim + 3) & ~3);
     const size_t terms = 8 * (size_t)group_batch(dim) * (size_t)group_tstride(dim);
-    return group_head_bytes(dim) + ((perm > terms ? perm : terms) + 15) / 16 * 16;
+    return ((perm > terms ? perm : terms) + 15) / 16 * 16;
 }
 
-__device__ inline GroupScratch group_scratch(unsigned char* base, int dim) {
+__host__ __device__ inline size_t group_scratch_bytes(int dim, bool stage = false) {
+    return group_head_bytes(dim) + group_union_bytes(dim) + ring_bytes(dim, stage);
+}
+
+__device__ inline GroupScratch group_scratch(unsigned char* base, int dim, bool stage = false) {
     GroupScratch g;
     g.dp = (dim + 3) & ~3;
     g.words = (dim + 31) / 32;
@@ -80,6 +133,14 @@ __device__ inline GroupScratch group_scratch(unsigned char* base, int dim) {
     g.bits = reinterpret_cast<unsigned*>(g.ws.pk + 2 * kMaxCachedPairs);
     g.perm = base + group_head_bytes(dim);
     g.T = reinterpret_cast<double*>(base + group_head_bytes(dim));
+    g.rld = ring_ld(dim);
+    if (stage) {
+        g.ring = reinterpret_cast<double*>(base + group_head_bytes(dim) + group_union_bytes(dim));
+        g.bar = reinterpret_cast<uint64_t*>(g.ring + (size_t)kStages * 4 * g.rld);
+    } else {
+        g.ring = nullptr;
+        g.bar = nullptr;
+    }
     g.ws.cand = g.ws.terms = nullptr;
     g.ws.head = g.ws.prev = g.ws.rj = nullptr;
     g.ws.bits = nullptr;
@@ -403,19 +464,20 @@ enum OutMode : int {
 // rows (T1, T2) and returns the finiteness vote.
 template <int MAXC, bool MANY, class Rows>
 __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, const Rows& R, int i, int p,
-                                       double* cand_out, double* T1, double* T2, const GroupScratch& g, int lane) {
+                                       double* cand_out, double* T1, double* T2, const GroupScratch& g, int lane,
+                                       const double* staged) {
     const int dim = P.dim;
     const int op = g.op[p];
     const int* sl = g.slot + 4 * p;
-    const double* x = R.at_key(sl[0]);
+    const double* x = staged ? staged : R.at_key(sl[0]);
     const double f = g.f[p];
     const bool many = MANY && op >= OP_AUTOTROPH;
     uint64_t base = 0;
     if (op != OP_AUTOTROPH || many) base = stream_base(P.seed, P.key_iteration, (uint64_t)i);
     if (many) group_extra_pairs(P, R, i, op, base, g, lane);
-    const double* xj = R.at_key(sl[op == OP_AUTOTROPH ? 1 : 0]);
-    const double* xm = R.at_key(sl[op >= OP_AUTOTROPH ? 2 : 0]);
-    const double* xp = R.at_key(sl[op >= OP_AUTOTROPH ? 3 : 0]);
+    const double* xj = staged ? staged + g.rld : R.at_key(sl[op == OP_AUTOTROPH ? 1 : 0]);
+    const double* xm = staged ? staged + 2 * g.rld : R.at_key(sl[op >= OP_AUTOTROPH ? 2 : 0]);
+    const double* xp = staged ? staged + 3 * g.rld : R.at_key(sl[op >= OP_AUTOTROPH ? 3 : 0]);
     const double w0 = g.w[p];
     const double sgn = g.sgn[p];
     const double npd = (double)P.npairs;
@@ -509,13 +571,36 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
                                     const uint8_t* in_dr_bytes, const unsigned* in_dr_bits, const double* p_dr,
                                     double* out_rows, double* out_fit, bool out_by_slot, uint8_t* out_acc,
                                     uint8_t* out_warn, uint8_t* sel_next, const GroupScratch& g, int lane,
-                                    unsigned long long& my_min, unsigned& my_warn) {
+                                    unsigned long long& my_min, unsigned& my_warn, unsigned* ring_phase = nullptr) {
     if (lane < n) {
         const int r0 = i0 - 1 + lane;
         const bool dr = in_dr_bits ? ((in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0 : in_dr_bytes[r0] != 0;
         group_phase_a(P, R, i0 + lane, dr, dr ? p_dr[r0] : 0.0, g, lane);
     }
     __syncwarp();
+    const bool staging = g.ring != nullptr;
+    // TMA prefetch of member p's rows into ring stage p % kStages (lane 0 issues).
+    auto issue = [&](int p) {
+        if (lane == 0) {
+            const int op = g.op[p];
+            const int nrows = op == OP_AUTOTROPH ? 4 : op == OP_HETEROTROPH ? 3 : op == OP_REPRODUCTION ? 1 : 0;
+            const int st = p % kStages;
+            double* dst = g.ring + (size_t)st * 4 * g.rld;
+            const unsigned bytes = (unsigned)(8 * P.ld);
+            fence_proxy_async();
+            mbar_expect_tx(&g.bar[st], bytes * (unsigned)nrows);
+            const int* sl = g.slot + 4 * p;
+            if (nrows >= 1) bulk_g2s(dst, R.at_key(sl[0]), bytes, &g.bar[st]);
+            if (nrows == 4) bulk_g2s(dst + g.rld, R.at_key(sl[1]), bytes, &g.bar[st]);
+            if (nrows >= 3) {
+                bulk_g2s(dst + 2 * g.rld, R.at_key(sl[2]), bytes, &g.bar[st]);
+                bulk_g2s(dst + 3 * g.rld, R.at_key(sl[3]), bytes, &g.bar[st]);
+            }
+        }
+    };
+    if (staging) {
+        for (int p = 0; p < kStages && p < n; p++) issue(p);
+    }
     const bool two = two_term_arrays(O.code);
     const int B = two ? g.batch / 2 : g.batch;
     double* T2base = g.T + (size_t)(g.batch / 2) * g.tstride;
@@ -530,9 +615,21 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
             else dst = out_rows + (size_t)(out_by_slot ? R.slot_of(own_key) : i - 1) * P.ld;
             double* T1 = g.T + (size_t)q * g.tstride;
             double* T2 = two ? T2base + (size_t)q * g.tstride : nullptr;
-            const bool ok = P.npairs > 1 ? group_candidate<MAXC, true>(P, O, R, i, p, dst, T1, T2, g, lane)
-                                          : group_candidate<MAXC, false>(P, O, R, i, p, dst, T1, T2, g, lane);
+            const double* staged = nullptr;
+            if (staging) {
+                const int st = p % kStages;
+                mbar_wait(&g.bar[st], (*ring_phase >> st) & 1u);
+                *ring_phase ^= 1u << st;
+                staged = g.ring + (size_t)st * 4 * g.rld;
+            }
+            const bool ok = P.npairs > 1
+                                ? group_candidate<MAXC, true>(P, O, R, i, p, dst, T1, T2, g, lane, staged)
+                                : group_candidate<MAXC, false>(P, O, R, i, p, dst, T1, T2, g, lane, staged);
             okmask |= (ok ? 1u : 0u) << q;
+            if (staging) {
+                __syncwarp();
+                if (p + kStages < n) issue(p + kStages);
+            }
         }
         __syncwarp();
         bool acc = false, warned = false;

@@ -206,7 +206,16 @@ __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group
     extern __shared__ __align__(16) unsigned char smem[];
     const IterParams& P = A.P;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const GroupScratch g = group_scratch(smem + (size_t)warp * group_scratch_bytes(P.dim), P.dim);
+    // SEL rows have an even stride (16-byte aligned) -> TMA-staged rows
+    constexpr bool kStage = SEL && MAXC > 0 && 32 * MAXC <= APO_STAGE_MAX_DIM;
+    const GroupScratch g =
+        group_scratch(smem + (size_t)warp * group_scratch_bytes(P.dim, kStage), P.dim, kStage);
+    unsigned ring_phase = 0;
+    if (kStage) {
+        if (lane < kStages) mbar_init(&g.bar[lane], 1);
+        mbar_fence_init();
+        __syncwarp();
+    }
     unsigned long long my_min = ~0ull;
     unsigned my_warn = 0;
     const int ngroups = (P.ps + 31) >> 5;
@@ -216,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group
         if constexpr (SEL) {
             const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
             update_group<MAXC, OUT_SEL>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
-                                        true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn);
+                                        true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn, &ring_phase);
         } else {
             const DenseSlots R{A.pos, A.fit, P.ld};
             update_group<MAXC, OUT_FIXUP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
@@ -428,8 +437,9 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
 }
 
 // MAXC >= 0: group path (apo_group.cuh); MAXC < 0: warp-per-protozoon (dim > 256).
+// 3 CTAs/SM: the C2 suite (360 runs) then fits one wave on 148 SMs.
 template <int MAXC>
-__global__ void __launch_bounds__(kThreads) k_run_batch(BatchArgs A) {
+__global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ unsigned long long red_min[32];
     __shared__ unsigned red_warn[32];
@@ -609,7 +619,8 @@ int launch_update(bool sel_mode, const UpdArgs& A, cudaStream_t st) {
     const int dim = A.P.dim;
     const bool group = dim <= kGroupMaxDim;
     const int w = group ? kWarps : warps_for_dim(dim);
-    const size_t smem = (group ? group_scratch_bytes(dim) : warp_scratch_bytes(dim)) * (size_t)w;
+    const bool stage = sel_mode && dim <= APO_STAGE_MAX_DIM;
+    const size_t smem = (group ? group_scratch_bytes(dim, stage) : warp_scratch_bytes(dim)) * (size_t)w;
     const void* fn = sel_mode ? pick_update_kernel<true>(dim) : pick_update_kernel<false>(dim);
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
