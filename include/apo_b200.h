@@ -43,12 +43,18 @@ extern "C" {
 #define APO_OBJ_ROSENBROCK 4
 #define APO_OBJ_GRIEWANK 5
 #define APO_OBJ_TABLE 6 /* table[round_half_up(x0)] (objectives.py:183-192, 213-219) */
+/* CEC2022 F1..F12: code = APO_OBJ_CEC2022_BASE + F (no reference counterpart,
+ * SPEC.md:146; definitions in csrc/apo_cec.cuh, data from cec2022.py). */
+#define APO_OBJ_CEC2022_BASE 100
 
 /* An objective as the kernels see it (device pointers). */
 typedef struct apo_objective {
     int32_t code;
     int32_t table_len;
-    const double *table;
+    const double *table;    /* elliptic weights / threshold table */
+    const double *shift;    /* CEC2022: [ncomp][dim] optima */
+    const double *rot_t;    /* CEC2022: [ncomp][dim][dim], rot_t[k][i][j] = M_k[j][i] */
+    const int32_t *shuffle; /* CEC2022 hybrids: [dim], 1-based */
 } apo_objective;
 
 int apo_abi_version(void);

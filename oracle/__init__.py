@@ -93,7 +93,32 @@ def _declare(L):
             fn.restype, fn.argtypes = spec
 
 
-_EXTRA_DECLS: dict = {}
+_EXTRA_DECLS: dict = {
+    "or_cec_eval_batch": (None, [C.c_int, _P, _I, C.c_int, _P, _P, _P, _P, C.c_int]),
+    "or_cec_spec": (None, [C.c_int, _P]),
+    "or_cec_ncomp": (C.c_int, [C.c_int]),
+}
+
+
+def cec_eval(fn: int, x, nthreads: int = 1) -> np.ndarray:
+    """CEC2022 F_fn on every row of x (CPU restatement, cec_oracle.c)."""
+    from paper_2510_14982_b200.cec2022 import cec_data
+
+    x = _f64(np.atleast_2d(x))
+    rows, dim = x.shape
+    shift, rot, shuffle = cec_data(fn, dim)
+    sh = np.ascontiguousarray(shift)
+    ro = np.ascontiguousarray(rot)
+    su = np.ascontiguousarray(shuffle, dtype=np.int32)
+    out = np.zeros(rows)
+    lib().or_cec_eval_batch(fn, _ptr(x), rows, dim, _ptr(sh), _ptr(ro), _ptr(su), _ptr(out), nthreads)
+    return out
+
+
+def cec_spec(fn: int) -> np.ndarray:
+    out = np.zeros(3 + 36)
+    lib().or_cec_spec(fn, _ptr(out))
+    return out
 
 
 def _ptr(a):
@@ -137,8 +162,19 @@ def elliptic_weights(dim: int) -> np.ndarray:
     return w
 
 
+def cec_packed(fn: int, dim: int, data_seed: int = 2022):
+    """Packed CEC2022 data [shift | rot | shuffle] for or_eval codes 100+F."""
+    from paper_2510_14982_b200.cec2022 import cec_data  # data synthesis only (numpy)
+
+    shift, rot, shuffle = cec_data(fn, dim, data_seed)
+    return np.concatenate([shift.ravel(), rot.ravel(), shuffle.astype(np.float64)])
+
+
 def objective_table(name: str, dim: int, table=None):
     """(code, table) the kernels read for a reference objective name."""
+    if name.startswith("cec2022_f"):
+        fn = int(name[len("cec2022_f"):])
+        return 100 + fn, cec_packed(fn, dim)
     code = CODES[name]
     if code == 2:
         return code, elliptic_weights(dim)

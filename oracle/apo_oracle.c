@@ -43,6 +43,21 @@
 #define PAIRS_BASE (1ULL << 33)
 #define COORD_INDEX 0xFFFFFFFFFFFFFFFFULL
 
+double or_cec_eval(int fn, const double *x, int n, const double *shift, const double *rot, const int *shuffle);
+int or_cec_ncomp(int fn);
+
+/* CEC2022 objectives (code 100+F, cec_oracle.c): `table` packs
+ * [shift ncomp*n][rot ncomp*n*n][shuffle n (as doubles)]. */
+static double cec_packed(int fn, const double *x, int64_t n, const double *table) {
+    int nc = or_cec_ncomp(fn);
+    const double *shift = table, *rot = table + (size_t)nc * n, *sh = rot + (size_t)nc * n * n;
+    int *shuffle = malloc(sizeof(int) * (size_t)n);
+    for (int64_t i = 0; i < n; i++) shuffle[i] = (int)sh[i];
+    double f = or_cec_eval(fn, x, (int)n, shift, rot, shuffle);
+    free(shuffle);
+    return f;
+}
+
 /* objective codes: objectives.py:34-42 */
 enum { SPHERE = 0, BENT_CIGAR = 1, ELLIPTIC = 2, HGBAT = 3, ROSENBROCK = 4, GRIEWANK = 5, TABLE = 6 };
 
@@ -84,6 +99,7 @@ void or_randperm(int64_t n, int64_t k, uint64_t base, uint64_t ctr0, int64_t *ou
  * ------------------------------------------------------------------------- */
 double or_eval(int64_t code, const double *x, int64_t n, const double *table, int64_t tlen) {
     double s, s1, s2, p;
+    if (code > 100) return cec_packed((int)(code - 100), x, n, table);
     switch (code) {
     case SPHERE:
         s = 0.0;

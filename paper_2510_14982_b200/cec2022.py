@@ -1,0 +1,97 @@
+"""CEC2022 F1-F12 objectives on synthetic data (no reference counterpart).
+
+The reference package implements only the six unshifted basic functions and
+lists the CEC shifted/rotated/hybrid/composition variants as a non-goal
+(SPEC.md:146); the official data files and C code are unavailable offline.
+This module therefore
+
+* restates the suite's structure (definitions live in csrc/apo_cec.cuh and,
+  as the test oracle, oracle/cec_oracle.c), and
+* synthesises the per-function data deterministically from (F, D, data_seed):
+  optima o_k ~ U[-80, 80]^D, Haar-orthogonal rotations M_k (QR of a Gaussian
+  with the R-diagonal sign fix), and a shuffle permutation for the hybrids.
+
+Known answers that need no official data: F(o) = F* for F1-F8 and the
+compositions' F(o_1) = F* (component 1 has bias 0 and takes all the weight).
+Every result here says "synthetic data" -- it is not comparable with
+published CEC2022 numbers.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+
+from .objectives import Objective, register_resolver
+
+CEC2022_BASE = 100
+CEC2022_NAMES = tuple(f"cec2022_f{k}" for k in range(1, 13))
+FSTAR = (300.0, 400.0, 600.0, 800.0, 900.0, 1800.0, 2000.0, 2200.0, 2300.0, 2400.0, 2600.0, 2700.0)
+NCOMP = (1, 1, 1, 1, 1, 1, 1, 1, 5, 3, 5, 6)  # shift vectors / rotations consumed
+HYBRID = (6, 7, 8)
+COMPOSITION = (9, 10, 11, 12)
+KIND = {**{k: "single" for k in range(1, 6)}, **{k: "hybrid" for k in HYBRID}, **{k: "composition" for k in COMPOSITION}}
+
+
+def _haar(rs: np.random.RandomState, d: int) -> np.ndarray:
+    a = rs.standard_normal((d, d))
+    q, r = np.linalg.qr(a)
+    return q * np.sign(np.diag(r))
+
+
+@lru_cache(maxsize=64)
+def cec_data(fn: int, dim: int, data_seed: int = 2022):
+    """(shift [ncomp, D], rot [ncomp, D, D], shuffle [D] 1-based) for F_fn at dimension D."""
+    if not 1 <= fn <= 12:
+        raise ValueError(f"CEC2022 function index must be 1..12, got {fn}")
+    if dim < 2:
+        raise ValueError("CEC2022 functions need dim >= 2")
+    rs = np.random.RandomState((data_seed * 1_000_003 + fn * 10_007 + dim) % (2 ** 32))
+    nc = NCOMP[fn - 1]
+    shift = rs.uniform(-80.0, 80.0, size=(nc, dim))
+    rot = np.stack([_haar(rs, dim) for _ in range(nc)])
+    shuffle = (rs.permutation(dim) + 1).astype(np.int32)
+    for a in (shift, rot, shuffle):
+        a.setflags(write=False)
+    return shift, rot, shuffle
+
+
+@dataclass(frozen=True)
+class CecFunction:
+    """Objective.data for a CEC2022 function: which F, and the data seed."""
+
+    fn: int
+    data_seed: int = 2022
+
+    def arrays(self, dim: int):
+        return cec_data(self.fn, dim, self.data_seed)
+
+    def optimum(self, dim: int) -> np.ndarray:
+        return self.arrays(dim)[0][0].copy()
+
+    @property
+    def fstar(self) -> float:
+        return FSTAR[self.fn - 1]
+
+
+# hybrids split D into ceil(p_k D)-sized segments; F7/F8 need D >= 5 for that to fit
+MIN_DIM = (2, 2, 2, 2, 2, 2, 5, 5, 2, 2, 2, 2)
+
+
+def cec2022_objective(fn: int, data_seed: int = 2022) -> Objective:
+    return Objective(f"cec2022_f{fn}", CEC2022_BASE + fn, min_dim=MIN_DIM[fn - 1], data=CecFunction(fn, data_seed))
+
+
+def _resolve(name: str):
+    key = name.strip().lower()
+    for prefix in ("cec2022_f", "cec2022-f", "f"):
+        if key.startswith(prefix) and key[len(prefix):].isdigit():
+            k = int(key[len(prefix):])
+            if 1 <= k <= 12 and (prefix != "f" or name.strip().upper().startswith("F")):
+                return cec2022_objective(k)
+    return None
+
+
+register_resolver(_resolve)

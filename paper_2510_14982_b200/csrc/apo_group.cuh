@@ -372,7 +372,11 @@ __device__ __forceinline__ double clampv(double c, double lo, double hi) {
     return c;
 }
 
-__device__ __forceinline__ bool two_term_arrays(int code) { return code == OBJ_HGBAT || code == OBJ_GRIEWANK; }
+// hgbat/griewank stage two term rows per protozoon; CEC objectives stage the
+// candidate itself and use the second half as rotation scratch.
+__device__ __forceinline__ bool two_term_arrays(int code) {
+    return code == OBJ_HGBAT || code == OBJ_GRIEWANK || code >= OBJ_CEC_BASE;
+}
 
 // Per-dimension fitness terms of candidate value c at dimension d (c_prev =
 // candidate value at d-1, valid when d >= 1).  Row T1 (and T2 for the
@@ -404,7 +408,9 @@ __device__ __forceinline__ void write_terms(const ObjDesc& O, double* T1, double
         T2[d] = cos(c / sqrt((double)d + 1.0));
         break;
     default:
-        if (d == 0) {
+        if (O.code >= OBJ_CEC_BASE) {
+            T1[d] = c;
+        } else if (d == 0) {
             long long idx = (long long)floor(c + 0.5);
             if (idx < 0) idx = 0;
             if (idx > O.table_len - 1) idx = O.table_len - 1;
@@ -633,6 +639,15 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
         }
         __syncwarp();
         bool acc = false, warned = false;
+        double cec_f = 0.0;
+        if (O.code >= OBJ_CEC_BASE) {  // warp-cooperative evaluation of each staged candidate
+            for (int q = 0; q < nb; q++) {
+                if (!((okmask >> q) & 1u)) continue;
+                const double fq = cec_eval_warp(O.cec, g.T + (size_t)q * g.tstride, T2base, T2base + g.tstride,
+                                                P.dim, lane);
+                if (lane == q) cec_f = fq;
+            }
+        }
         if (lane < nb) {
             const int p = h + lane, i = i0 + p;
             const int own_key = g.slot[4 * p];
@@ -640,8 +655,10 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
             const double fit_i = R.fit_at(own);
             double kept = fit_i;
             if ((okmask >> lane) & 1u) {
-                const double nf = fold_terms(O, g.T + (size_t)lane * g.tstride,
-                                             two ? T2base + (size_t)lane * g.tstride : nullptr, P.dim);
+                const double nf = O.code >= OBJ_CEC_BASE
+                                      ? cec_f
+                                      : fold_terms(O, g.T + (size_t)lane * g.tstride,
+                                                   two ? T2base + (size_t)lane * g.tstride : nullptr, P.dim);
                 if (isfinite(nf)) {
                     acc = nf < fit_i;
                     if (acc) kept = nf;

@@ -85,12 +85,23 @@ ObjDesc to_desc(const apo_objective* o) {
     d.code = o->code;
     d.table_len = o->table_len;
     d.table = o->table;
+    d.cec.fn = o->code >= APO_OBJ_CEC2022_BASE ? o->code - APO_OBJ_CEC2022_BASE : 0;
+    d.cec.shift = o->shift;
+    d.cec.rot_t = o->rot_t;
+    d.cec.shuffle = o->shuffle;
     return d;
 }
 
 int check_objective(const apo_objective* o, int64_t dim) {
     APO_CHECK(o != nullptr, "objective descriptor is NULL");
-    APO_CHECK(o->code >= APO_OBJ_SPHERE && o->code <= APO_OBJ_TABLE, "unsupported objective code");
+    const bool cec = o->code > APO_OBJ_CEC2022_BASE && o->code <= APO_OBJ_CEC2022_BASE + 12;
+    APO_CHECK(cec || (o->code >= APO_OBJ_SPHERE && o->code <= APO_OBJ_TABLE), "unsupported objective code");
+    if (cec) {
+        APO_CHECK(o->shift && o->rot_t, "CEC2022 objectives need shift and rotation data");
+        const int fn = o->code - APO_OBJ_CEC2022_BASE;
+        APO_CHECK(fn < 6 || fn > 8 || o->shuffle, "CEC2022 hybrid functions need a shuffle");
+        APO_CHECK(dim >= ((fn == 7 || fn == 8) ? 5 : 2), "CEC2022 dim too small (F7/F8 need >= 5, others >= 2)");
+    }
     if (o->code == APO_OBJ_ELLIPTIC) APO_CHECK(o->table && o->table_len >= dim, "elliptic needs dim weights");
     if (o->code == APO_OBJ_TABLE) APO_CHECK(o->table && o->table_len >= 1, "table objective needs a table");
     return APO_OK;
@@ -253,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) k_init(uint64_t seed, int ps, int di
             row[d] = c;
         }
         __syncwarp();
-        const double f = eval_warp(O, s.cand, s.terms, dim, lane);
+        const double f = eval_warp(O, s.cand, s.terms, dim, lane, s.aux);
         if (lane == 0) fit[r0] = f;
         const unsigned long long k = sort_key(f);
         my_min = k < my_min ? k : my_min;
@@ -276,7 +287,7 @@ __global__ void __launch_bounds__(kThreads) k_evaluate(const double* __restrict_
         const double* row = x + (size_t)r0 * ld;
         for (int d = lane; d < dim; d += 32) s.cand[d] = row[d];
         __syncwarp();
-        const double f = eval_warp(O, s.cand, s.terms, dim, lane);
+        const double f = eval_warp(O, s.cand, s.terms, dim, lane, s.aux);
         if (lane == 0) out[r0] = f;
     }
 }
@@ -408,7 +419,10 @@ struct BatchLayout {
 };
 
 __host__ __device__ inline size_t batch_warp_bytes(int dim) {
-    return dim <= kGroupMaxDim ? group_scratch_bytes(dim) : warp_scratch_bytes(dim);
+    const size_t ws = warp_scratch_bytes(dim);  // init + warp path
+    if (dim > kGroupMaxDim) return ws;
+    const size_t gs = group_scratch_bytes(dim);
+    return gs > ws ? gs : ws;
 }
 
 __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int nwarps) {
@@ -475,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
         __syncwarp();
         for (int d = lane; d < dim; d += 32) iws.cand[d] = row[d];
         __syncwarp();
-        const double f = eval_warp(O, iws.cand, iws.terms, dim, lane);
+        const double f = eval_warp(O, iws.cand, iws.terms, dim, lane, iws.aux);
         if (lane == 0) {
             fit[0][r0] = f;
             keys[r0] = sort_key(f);

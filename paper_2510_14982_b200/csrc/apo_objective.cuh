@@ -6,6 +6,7 @@
 // the reference) and lane 0 then accumulates them in order, so the sum is
 // bit-identical.  Table lookup: objectives.py:213-219.
 #pragma once
+#include "apo_cec.cuh"
 #include "apo_device.cuh"
 
 namespace apo {
@@ -25,6 +26,7 @@ struct ObjDesc {
     int code;
     int table_len;
     const double* table;  // elliptic weights (code 2) or value table (code 6)
+    CecData cec;          // CEC2022 data (code OBJ_CEC_BASE + F)
 };
 
 __device__ __forceinline__ double warp_bcast(double v, int src) { return __shfl_sync(0xFFFFFFFFu, v, src); }
@@ -45,10 +47,12 @@ __device__ __forceinline__ double seq_sum(const double* t, int from, int to) {
     return s;
 }
 
-// c: candidate [dim] (shared), t: scratch [dim] (shared).  Returns the
+// c: candidate [dim] (shared), t / aux: scratch [dim] (shared).  Returns the
 // fitness on every lane.
-__device__ inline double eval_warp(const ObjDesc& O, const double* c, double* t, int dim, int lane) {
+__device__ inline double eval_warp(const ObjDesc& O, const double* c, double* t, int dim, int lane,
+                                   double* aux = nullptr) {
     double f = 0.0;
+    if (O.code >= OBJ_CEC_BASE) return cec_eval_warp(O.cec, c, t, aux, dim, lane);
     switch (O.code) {
     case OBJ_SPHERE:
         for (int d = lane; d < dim; d += 32) t[d] = c[d] * c[d];

@@ -37,6 +37,7 @@ struct IterParams {
 struct WarpScratch {
     double* cand;    // [dim] candidate, then the kept row
     double* terms;   // [dim] per-dimension fitness terms
+    double* aux;     // [dim] second scratch row (CEC rotation output)
     int* head;       // [dim] latest mask step that hit a position
     int* prev;       // [dim] previous step hitting the same position
     int* rj;         // [dim] swap targets r_j of the partial Fisher-Yates
@@ -48,7 +49,7 @@ struct WarpScratch {
 __host__ __device__ inline size_t warp_scratch_bytes(int dim) {
     const size_t d2 = (size_t)((dim + 1) & ~1);
     size_t words = (size_t)(dim + 31) / 32;
-    size_t b = 16 * d2 + 12 * (size_t)dim + 4 * words + 8 * kMaxCachedPairs + 8 * kMaxCachedPairs;
+    size_t b = 24 * d2 + 12 * (size_t)dim + 4 * words + 8 * kMaxCachedPairs + 8 * kMaxCachedPairs;
     return (b + 15) & ~(size_t)15;
 }
 
@@ -58,7 +59,8 @@ __device__ inline WarpScratch warp_scratch(unsigned char* base, int dim) {
     const int d2 = (dim + 1) & ~1;
     s.cand = reinterpret_cast<double*>(base);
     s.terms = s.cand + d2;
-    s.pw = s.terms + d2;
+    s.aux = s.terms + d2;
+    s.pw = s.aux + d2;
     s.head = reinterpret_cast<int*>(s.pw + kMaxCachedPairs);
     s.prev = s.head + dim;
     s.rj = s.prev + dim;
@@ -296,7 +298,7 @@ __device__ inline UpdateResult update_protozoon(const IterParams& P, const ObjDe
     res.warned = false;
     res.fitness = fit_i;
     if (ok) {
-        const double nf = eval_warp(O, s.cand, s.terms, dim, lane);
+        const double nf = eval_warp(O, s.cand, s.terms, dim, lane, s.aux);
         if (isfinite(nf)) {
             res.accepted = nf < fit_i;
             if (res.accepted) res.fitness = nf;

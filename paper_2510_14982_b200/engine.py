@@ -110,6 +110,28 @@ def _dev():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def _to_device(arr: np.ndarray, dev):
+    """Host array -> device tensor; page-locked arrays (from _to_host) copy asynchronously at full PCIe rate."""
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    return t.to(dev, non_blocking=t.is_pinned())
+
+
+def _to_host(*tensors):
+    """Device tensors -> numpy arrays backed by page-locked host memory (torch's caching host
+    allocator), so a Population returned here can be fed back to step() without a staging copy."""
+    import torch
+
+    outs = []
+    for t in tensors:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in outs]
+
+
 def initialize(cfg: ApoConfig, objective) -> Population:
     """Iteration-0 population on the device (engine.py:116-139); fe_count = ps."""
     import torch
@@ -124,7 +146,8 @@ def initialize(cfg: ApoConfig, objective) -> Population:
     dobj = device_objective(obj, cfg.dim)
     _lib.check(lib.apo_initialize(cfg.seed, cfg.ps, cfg.dim, cfg.dim, cfg.bounds.lower, cfg.bounds.span, dobj.ref,
                                   _lib.ptr(pos), _lib.ptr(fit), _lib.stream_handle()), "apo_initialize")
-    return Population(pos.cpu().numpy(), fit.cpu().numpy(), iteration=0, fe_count=cfg.ps, warnings=0)
+    hp, hf = _to_host(pos, fit)
+    return Population(hp, hf, iteration=0, fe_count=cfg.ps, warnings=0)
 
 
 def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: EngineMode = None,
@@ -142,8 +165,8 @@ def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: Engin
     lib = _lib.require_cuda()
     dev = _dev()
     stream = _lib.stream_handle()
-    pos = torch.as_tensor(pop.positions, device=dev)
-    fit = torch.as_tensor(pop.fitness, device=dev)
+    pos = _to_device(pop.positions, dev)
+    fit = _to_device(pop.fitness, dev)
     order = torch.empty(cfg.ps, dtype=torch.int32, device=dev)
     _lib.check(lib.apo_sort_order(_lib.ptr(fit), cfg.ps, _lib.ptr(order), stream), "apo_sort_order")
     order = order.long()
@@ -154,8 +177,9 @@ def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: Engin
                "apo_select_dr")
     new_pos, new_fit, _acc, warned = bk.run_updates(snap_pos, snap_fit, in_dr, cfg, obj, iteration, iteration + 1,
                                                     parallel=(mode.kind == PARALLEL), workers=workers)
-    return Population(new_pos.cpu().numpy(), new_fit.cpu().numpy(), iteration=iteration + 1,
-                      fe_count=pop.fe_count + cfg.ps, warnings=pop.warnings + warned)
+    hp, hf = _to_host(new_pos, new_fit)
+    return Population(hp, hf, iteration=iteration + 1, fe_count=pop.fe_count + cfg.ps,
+                      warnings=pop.warnings + warned)
 
 
 # ---------------------------------------------------------------------------

@@ -164,10 +164,15 @@ class DeviceObjective:
             table = np.asarray(elliptic_weights(dim))
         elif obj.code == TABLE:
             table = obj.table
-        elif obj.data is not None and hasattr(obj.data, "device_table"):
-            table = obj.data.device_table(dim)
         self.struct = _lib.apo_objective()
         self.struct.code = int(obj.code)
+        if obj.data is not None and hasattr(obj.data, "arrays"):  # CEC2022
+            shift, rot, shuffle = obj.data.arrays(dim)
+            rot_t = np.ascontiguousarray(np.transpose(rot, (0, 2, 1)))
+            for field, arr in (("shift", shift), ("rot_t", rot_t), ("shuffle", shuffle)):
+                t = torch.as_tensor(np.array(arr), device=dev)
+                self.keep.append(t)
+                setattr(self.struct, field, t.data_ptr())
         if table is not None:
             t = torch.as_tensor(np.array(table, dtype=np.float64), device=dev)
             self.keep.append(t)
