@@ -24,7 +24,9 @@ ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # --fmad=false: oracle-exact arithmetic (the reference never fuses mul+add).
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
               "-diag-suppress", "177"]
-SOURCES = ["apo_kernels.cu"]
+# One TU per kernel family so nvcc runs in parallel (the templates live in
+# csrc/apo_kernels.cuh); linked into a single shared library.
+SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_batch.cu"]
 
 _lock = threading.Lock()
 _lib = None
@@ -50,18 +52,36 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libapo_b200.so for sm_100a (in-tree, so it travels with the repo)."""
+    """Compile libapo_b200.so for sm_100a (in-tree, so it travels with the repo).
+
+    Each TU compiles to an object in parallel, then nvcc links the shared
+    library."""
+    from concurrent.futures import ThreadPoolExecutor
+
     with _lock:
         if not force and not _stale():
             return LIB_PATH
+        objdir = os.path.join(PKG_DIR, "build")
+        os.makedirs(objdir, exist_ok=True)
+        flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+        def compile_one(src):
+            obj = os.path.join(objdir, src.replace(".cu", ".o"))
+            cmd = [nvcc(), *ARCH_FLAGS, *flags, "-I", INCLUDE, "-I", CSRC, "-c", "-o", obj, os.path.join(CSRC, src)]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            results = list(ex.map(compile_one, SOURCES))
+        for obj, proc in results:
+            if proc.returncode != 0:
+                raise ApoError(f"nvcc failed for {obj} ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
         tmp = LIB_PATH + ".tmp"
-        cmd = [nvcc(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp,
-               *[os.path.join(CSRC, s) for s in SOURCES]]
-        if verbose:
-            print(" ".join(cmd))
+        cmd = [nvcc(), *ARCH_FLAGS, "-shared", "-o", tmp, *[o for o, _ in results]]
         proc = subprocess.run(cmd, capture_output=True, text=True)
         if proc.returncode != 0:
-            raise ApoError(f"nvcc failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
+            raise ApoError(f"nvcc link failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
         os.replace(tmp, LIB_PATH)
         return LIB_PATH
 

@@ -1,0 +1,377 @@
+// apo_kernels.cuh -- kernel templates shared by the translation units of libapo_b200.so.
+//
+// The update and batch kernels are instantiated in their own TUs
+// (apo_update_sel.cu, apo_update_dense.cu, apo_batch.cu) so the library
+// builds in parallel; apo_kernels.cu holds the small kernels and the C ABI
+// and reaches the templates through the pick_* getters below.
+#pragma once
+#include <cstdint>
+#include "apo_group.cuh"
+#include "apo_update.cuh"
+
+namespace apo {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// ---------------------------------------------------------------------------
+// Update launch arguments.  SEL mode (device-resident loop): rows live in
+// pos0/pos1 selected per slot by sel[], ranks map to slots through order[],
+// candidates go to the alternate buffer and sel_next/out_fit (by slot)
+// record what is kept.  Dense mode (run_updates boundary): rank-ordered rows
+// in pos -> out_pos, out_fit/out_acc/out_warn by rank.
+struct UpdArgs {
+    IterParams P;
+    ObjDesc O;
+    const double* pos0;
+    const double* pos1;
+    const uint8_t* sel;
+    uint8_t* sel_next;
+    const double* pos;
+    double* out_pos;
+    const double* fit;
+    const int* order;
+    double* out_fit;
+    const uint8_t* in_dr_bytes;
+    const unsigned* in_dr_bits;
+    const double* p_dr;
+    uint8_t* out_acc;
+    uint8_t* out_warn;
+    unsigned long long* warn_count;
+    unsigned long long* trace_key;
+};
+
+__device__ __forceinline__ void block_finish(unsigned long long my_min, unsigned my_warn,
+                                             unsigned long long* warn_count, unsigned long long* trace_key) {
+    __shared__ unsigned long long red_min[32];
+    __shared__ unsigned red_warn[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long m2 = __shfl_xor_sync(kFull, my_min, o);
+        my_min = m2 < my_min ? m2 : my_min;
+        my_warn += __shfl_xor_sync(kFull, my_warn, o);
+    }
+    if (lane == 0) {
+        red_min[warp] = my_min;
+        red_warn[warp] = my_warn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long m = ~0ull;
+        unsigned w = 0;
+        for (int k = 0; k < nwarps; k++) {
+            m = red_min[k] < m ? red_min[k] : m;
+            w += red_warn[k];
+        }
+        if (trace_key && m != ~0ull) atomicMin(trace_key, m);
+        if (warn_count && w) atomicAdd(warn_count, (unsigned long long)w);
+    }
+}
+
+// Warp-per-protozoon path (dim > 256).
+template <bool SEL>
+__global__ void __launch_bounds__(kThreads) k_update(UpdArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const IterParams& P = A.P;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const WarpScratch s = warp_scratch(smem + (size_t)warp * warp_scratch_bytes(P.dim), P.dim);
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    for (int r0 = blockIdx.x * nwarps + warp; r0 < P.ps; r0 += gridDim.x * nwarps) {
+        const bool dr = A.in_dr_bits ? ((A.in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0 : A.in_dr_bytes[r0] != 0;
+        const double pdr = dr ? A.p_dr[r0] : 0.0;
+        UpdateResult res;
+        if constexpr (SEL) {
+            const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
+            const int slot = A.order[r0];
+            res = update_protozoon(P, A.O, R, r0 + 1, dr, pdr, R.alt(slot), s, lane);
+            if (lane == 0) {
+                A.out_fit[slot] = res.fitness;
+                A.sel_next[slot] = A.sel[slot] ^ 1;  // the full kept row went to the alternate buffer
+            }
+        } else {
+            const DenseRows R{A.pos, A.fit, P.ld};
+            res = update_protozoon(P, A.O, R, r0 + 1, dr, pdr, A.out_pos + (size_t)r0 * P.ld, s, lane);
+            if (lane == 0) {
+                A.out_fit[r0] = res.fitness;
+                if (A.out_acc) A.out_acc[r0] = res.accepted ? 1 : 0;
+                if (A.out_warn) A.out_warn[r0] = res.warned ? 1 : 0;
+            }
+        }
+        if (lane == 0) {
+            const unsigned long long k = sort_key(res.fitness);
+            my_min = k < my_min ? k : my_min;
+            my_warn += res.warned ? 1u : 0u;
+        }
+    }
+    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
+}
+
+// Group path (dim <= 256): one warp per 32 consecutive ranks, see apo_group.cuh.
+#ifndef APO_GROUP_MIN_BLOCKS
+#define APO_GROUP_MIN_BLOCKS 2
+#endif
+template <bool SEL, int MAXC>
+__global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group(UpdArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const IterParams& P = A.P;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    // SEL rows have an even stride (16-byte aligned) -> TMA-staged rows
+    constexpr bool kStage = SEL && MAXC > 0 && 32 * MAXC <= APO_STAGE_MAX_DIM;
+    const GroupScratch g =
+        group_scratch(smem + (size_t)warp * group_scratch_bytes(P.dim, kStage), P.dim, kStage);
+    unsigned ring_phase = 0;
+    if (kStage) {
+        if (lane < kStages) mbar_init(&g.bar[lane], 1);
+        mbar_fence_init();
+        __syncwarp();
+    }
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    const int ngroups = (P.ps + 31) >> 5;
+    for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
+        const int i0 = grp * 32 + 1;
+        const int n = min(32, P.ps - grp * 32);
+        if constexpr (SEL) {
+            const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
+            update_group<MAXC, OUT_SEL>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
+                                        true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn, &ring_phase);
+        } else {
+            const DenseSlots R{A.pos, A.fit, P.ld};
+            update_group<MAXC, OUT_FIXUP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
+                                          A.out_fit, false, A.out_acc, A.out_warn, nullptr, g, lane, my_min,
+                                          my_warn);
+        }
+    }
+    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent batched runs: one CTA = one independent run, resident in SMEM.
+struct BatchArgs {
+    const uint64_t* seeds;
+    const ObjDesc* objs;
+    int ps, dim, ld, max_iterations, n_iters, npairs;
+    double pf_max, lower, upper, span, eps;
+    const double* sched;  // [max_iterations][3]
+    const double* p_dr;   // [ps]
+    double* best_fit;
+    double* best_pos;
+    double* trace;
+    double* final_pos;
+    double* final_fit;
+    long long* warnings;
+};
+
+struct BatchLayout {
+    size_t pos0, pos1, fit0, fit1, keys, order, rankof, newrank, chead, cprev, crj, cbits, warps, total;
+};
+
+__host__ __device__ inline size_t batch_warp_bytes(int dim) {
+    const size_t ws = warp_scratch_bytes(dim);  // init + warp path
+    if (dim > kGroupMaxDim) return ws;
+    const size_t gs = group_scratch_bytes(dim);
+    return gs > ws ? gs : ws;
+}
+
+__host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int nwarps) {
+    BatchLayout L;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o += (bytes + 15) & ~(size_t)15;
+        return at;
+    };
+    L.pos0 = take(8 * (size_t)ps * ld);
+    L.pos1 = take(8 * (size_t)ps * ld);
+    L.fit0 = take(8 * (size_t)ps);
+    L.fit1 = take(8 * (size_t)ps);
+    L.keys = take(8 * (size_t)ps);
+    L.order = take(4 * (size_t)ps);
+    L.rankof = take(4 * (size_t)ps);
+    L.newrank = take(4 * (size_t)ps);
+    L.chead = take(4 * (size_t)ps);
+    L.cprev = take(4 * (size_t)ps);
+    L.crj = take(4 * (size_t)ps);
+    L.cbits = take(4 * (size_t)((ps + 31) / 32));
+    L.warps = take(batch_warp_bytes(dim) * (size_t)nwarps);
+    L.total = o;
+    return L;
+}
+
+// MAXC >= 0: group path (apo_group.cuh); MAXC < 0: warp-per-protozoon (dim > 256).
+// 3 CTAs/SM: the C2 suite (360 runs) then fits one wave on 148 SMs.
+template <int MAXC>
+__global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned long long red_min[32];
+    __shared__ unsigned red_warn[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int run = blockIdx.x;
+    const int ps = A.ps, dim = A.dim, ld = A.ld;
+    const BatchLayout L = batch_layout(ps, dim, ld, nwarps);
+    double* pos[2] = {reinterpret_cast<double*>(smem + L.pos0), reinterpret_cast<double*>(smem + L.pos1)};
+    double* fit[2] = {reinterpret_cast<double*>(smem + L.fit0), reinterpret_cast<double*>(smem + L.fit1)};
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + L.keys);
+    int* order = reinterpret_cast<int*>(smem + L.order);
+    int* rankof = reinterpret_cast<int*>(smem + L.rankof);
+    int* newrank = reinterpret_cast<int*>(smem + L.newrank);
+    WarpScratch cs;
+    cs.head = reinterpret_cast<int*>(smem + L.chead);
+    cs.prev = reinterpret_cast<int*>(smem + L.cprev);
+    cs.rj = reinterpret_cast<int*>(smem + L.crj);
+    cs.bits = reinterpret_cast<unsigned*>(smem + L.cbits);
+    unsigned char* wbase = smem + L.warps + (size_t)warp * batch_warp_bytes(dim);
+    const GroupScratch g = group_scratch(wbase, dim);
+    const WarpScratch ws = MAXC >= 0 ? g.ws : warp_scratch(wbase, dim);
+    const uint64_t seed = A.seeds[run];
+    const ObjDesc O = A.objs[run];
+    double* trace = A.trace ? A.trace + (size_t)run * (A.n_iters + 1) : nullptr;
+
+    // initialisation (engine.py:116-139); the init scratch aliases this warp's group scratch
+    unsigned long long my_min = ~0ull;
+    const WarpScratch iws = warp_scratch(wbase, dim);
+    for (int r0 = warp; r0 < ps; r0 += nwarps) {
+        const uint64_t base = stream_base(seed, 0, (uint64_t)(r0 + 1));
+        double* row = pos[0] + (size_t)r0 * ld;
+        for (int d = lane; d < dim; d += 32) row[d] = A.lower + uniform(base, (uint64_t)d) * A.span;
+        __syncwarp();
+        for (int d = lane; d < dim; d += 32) iws.cand[d] = row[d];
+        __syncwarp();
+        const double f = eval_warp(O, iws.cand, iws.terms, dim, lane, iws.aux);
+        if (lane == 0) {
+            fit[0][r0] = f;
+            keys[r0] = sort_key(f);
+            order[r0] = r0;
+            rankof[r0] = r0;
+            my_min = sort_key(f) < my_min ? sort_key(f) : my_min;
+        }
+    }
+    if (lane == 0) red_min[warp] = my_min;
+    __syncthreads();
+    if (threadIdx.x == 0 && trace) {
+        unsigned long long m = ~0ull;
+        for (int k = 0; k < nwarps; k++) m = red_min[k] < m ? red_min[k] : m;
+        trace[0] = key_to_double(m);
+    }
+    unsigned warn_total = 0;
+    int cur = 0;
+    for (int t = 0; t < A.n_iters; t++) {
+        // 1. stable sort by fitness, ties by previous rank (core.py:504-513)
+        for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) {
+            const unsigned long long k = keys[sl];
+            const int pr = rankof[sl];
+            int cnt = 0;
+            for (int q = 0; q < ps; q++) {
+                const unsigned long long kq = keys[q];
+                cnt += (kq < k) || (kq == k && rankof[q] < pr);
+            }
+            newrank[sl] = cnt;
+        }
+        __syncthreads();
+        for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) {
+            order[newrank[sl]] = sl;
+            rankof[sl] = newrank[sl];
+        }
+        // 2. coordinator draws (core.py:263-278)
+        const uint64_t key_it = (uint64_t)t + 1;
+        if (warp == 0) {
+            const uint64_t cbase = stream_base(seed, key_it, kCoordinator);
+            const double pf = A.pf_max * uniform(cbase, 0);
+            const int count = (int)ceil((double)ps * pf);
+            build_mask(ps, count, cbase, 1, cs, lane);
+        }
+        __syncthreads();
+        // 3. fused updates
+        IterParams P;
+        P.seed = seed;
+        P.key_iteration = key_it;
+        P.ps = ps;
+        P.dim = dim;
+        P.npairs = A.npairs;
+        P.ld = ld;
+        P.lower = A.lower;
+        P.upper = A.upper;
+        P.span = A.span;
+        P.eps = A.eps;
+        P.p_ah = A.sched[3 * t];
+        P.f_mult = A.sched[3 * t + 1];
+        P.decay = A.sched[3 * t + 2];
+        const int nxt = cur ^ 1;
+        my_min = ~0ull;
+        unsigned my_warn = 0;
+        if constexpr (MAXC >= 0) {
+            const OrderedSlots R{pos[cur], fit[cur], order, ld};
+            const int G = min(32, (ps + nwarps - 1) / nwarps);
+            for (int q = warp; q * G < ps; q += nwarps) {
+                const int i0 = q * G + 1;
+                update_group<MAXC, OUT_FIXUP>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr, pos[nxt],
+                                              fit[nxt], true, nullptr, nullptr, nullptr, g, lane, my_min, my_warn);
+            }
+            __syncthreads();
+            for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) keys[sl] = sort_key(fit[nxt][sl]);
+        } else {
+            const OrderedRows R{pos[cur], fit[cur], order, ld};
+            for (int r0 = warp; r0 < ps; r0 += nwarps) {
+                const bool dr = ((cs.bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0;
+                const int slot = order[r0];
+                const UpdateResult res = update_protozoon(P, O, R, r0 + 1, dr, dr ? A.p_dr[r0] : 0.0,
+                                                          pos[nxt] + (size_t)slot * ld, ws, lane);
+                if (lane == 0) {
+                    fit[nxt][slot] = res.fitness;
+                    const unsigned long long k = sort_key(res.fitness);
+                    keys[slot] = k;
+                    my_min = k < my_min ? k : my_min;
+                    my_warn += res.warned ? 1u : 0u;
+                }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long m2 = __shfl_xor_sync(kFull, my_min, o);
+            my_min = m2 < my_min ? m2 : my_min;
+            my_warn += __shfl_xor_sync(kFull, my_warn, o);
+        }
+        if (lane == 0) {
+            red_min[warp] = my_min;
+            red_warn[warp] = my_warn;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long m = ~0ull;
+            for (int k = 0; k < nwarps; k++) {
+                m = red_min[k] < m ? red_min[k] : m;
+                warn_total += red_warn[k];
+            }
+            if (trace) trace[t + 1] = key_to_double(m);
+        }
+        cur = nxt;
+        __syncthreads();
+    }
+    // outputs in reference row order (row r = order[r])
+    if (threadIdx.x == 0) {
+        int best = 0;
+        for (int r = 1; r < ps; r++)
+            if (fit[cur][order[r]] < fit[cur][order[best]]) best = r;
+        red_warn[0] = (unsigned)best;
+        A.best_fit[run] = fit[cur][order[best]];
+        if (A.warnings) A.warnings[run] = warn_total;
+    }
+    __syncthreads();
+    const int bslot = order[red_warn[0]];
+    if (A.best_pos)
+        for (int d = threadIdx.x; d < dim; d += blockDim.x) A.best_pos[(size_t)run * dim + d] = pos[cur][(size_t)bslot * ld + d];
+    if (A.final_pos)
+        for (int e = threadIdx.x; e < ps * dim; e += blockDim.x) {
+            const int r = e / dim, d = e - r * dim;
+            A.final_pos[(size_t)run * ps * dim + e] = pos[cur][(size_t)order[r] * ld + d];
+        }
+    if (A.final_fit)
+        for (int r = threadIdx.x; r < ps; r += blockDim.x) A.final_fit[(size_t)run * ps + r] = fit[cur][order[r]];
+}
+
+// Kernel getters (defined in the instantiating TUs).
+const void* pick_update_sel(int dim);
+const void* pick_update_dense(int dim);
+const void* pick_run_batch(int dim);
+
+}  // namespace apo
