@@ -55,6 +55,11 @@ typedef struct apo_objective {
     const double *shift;    /* CEC2022: [ncomp][dim] optima */
     const double *rot_t;    /* CEC2022: [ncomp][dim][dim], rot_t[k][i][j] = M_k[j][i] */
     const int32_t *shuffle; /* CEC2022 hybrids: [dim], 1-based */
+    /* CEC2022, optional: rot_t zero-padded to [ncomp][round_up(dim,4)][8*nt]
+     * with nt = dim<=16 ? 2 : dim<=32 ? 4 : dim<=56 ? 7 : 13 (dim <= 104).
+     * When present, large populations evaluate in the DMMA kernel
+     * k_cec_eval; table may then hold the ELLIPS weights 10^(6i/(dim-1)). */
+    const double *rot_pad;
 } apo_objective;
 
 int apo_abi_version(void);
@@ -139,6 +144,9 @@ int apo_run_destroy(apo_run *run);
  * since the last apo_run_profile call. */
 int apo_run_profile(apo_run *run, int enable);
 int apo_run_profile_read(apo_run *run, double *update_ms_host, int64_t *launches_host);
+/* Same, split at the boundary between the candidate kernel and the CEC2022
+ * evaluation kernel (k_cec_eval; evaluate_ms is 0 for fused objectives). */
+int apo_run_profile_split(apo_run *run, double *candidates_ms_host, double *evaluate_ms_host, int64_t *launches_host);
 
 /*
  * Many independent small runs, one CTA per run, the whole run resident in

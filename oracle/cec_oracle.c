@@ -321,12 +321,15 @@ void or_cec_spec(int fn, double *out) {
     }
 }
 
-/* Hybrid segment sizes: ceil(p_i * n) for i < N-1, remainder last. */
+/* Hybrid segment sizes: ceil(p_i * n) for i < N-1, remainder last.  At
+ * dimensions where the rounded-up sizes would exceed n (e.g. F7 at n = 12)
+ * a segment is cut at n so every segment stays inside the candidate. */
 void or_cec_segments(int fn, int n, int *sizes) {
     const cec_spec *S = &SPECS[fn - 1];
     int tot = 0;
     for (int c = 0; c < S->ncomp - 1; c++) {
         sizes[c] = (int)ceil(S->p[c] * n);
+        if (sizes[c] > n - tot) sizes[c] = n - tot;
         tot += sizes[c];
     }
     sizes[S->ncomp - 1] = n - tot;

@@ -26,7 +26,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-
               "-diag-suppress", "177"]
 # One TU per kernel family so nvcc runs in parallel (the templates live in
 # csrc/apo_kernels.cuh); linked into a single shared library.
-SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_batch.cu"]
+SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_batch.cu", "apo_cec_eval.cu"]
 
 _lock = threading.Lock()
 _lib = None
@@ -95,7 +95,7 @@ _INT = C.c_int
 
 class apo_objective(C.Structure):
     _fields_ = [("code", C.c_int32), ("table_len", C.c_int32), ("table", C.c_void_p), ("shift", C.c_void_p),
-                ("rot_t", C.c_void_p), ("shuffle", C.c_void_p)]
+                ("rot_t", C.c_void_p), ("shuffle", C.c_void_p), ("rot_pad", C.c_void_p)]
 
 
 PROTOTYPES = {
@@ -122,6 +122,7 @@ PROTOTYPES = {
     "apo_run_destroy": (_INT, [_P]),
     "apo_run_profile": (_INT, [_P, _INT]),
     "apo_run_profile_read": (_INT, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "apo_run_profile_split": (_INT, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "apo_run_batch": (_INT, [_I, _P, C.POINTER(apo_objective), _I, _I, _I, _I, _I, _D, _D, _D, _D, _P, _P, _P, _P,
                              _P, _P, _P, _P, _P]),
     "apo_run_batch_max_elems": (_I, [_I, _I]),

@@ -246,10 +246,11 @@ __device__ __forceinline__ void cec_rotate(const double* __restrict__ rot_t, con
 }
 
 struct CecData {
-    int fn;                // 1..12
-    const double* shift;   // [ncomp][n]
-    const double* rot_t;   // [ncomp][n][n]
-    const int* shuffle;    // [n] (1-based)
+    int fn;                 // 1..12
+    const double* shift;    // [ncomp][n]
+    const double* rot_t;    // [ncomp][n][n]
+    const int* shuffle;     // [n] (1-based)
+    const double* rot_pad;  // [ncomp][n4][8 NT] zero-padded rot_t (k_cec_eval), nullable
 };
 
 // F_fn(c) for a candidate c[0..n) in shared memory; y, z: shared scratch [n].
@@ -280,6 +281,7 @@ __device__ inline double cec_eval_warp(const CecData& C, const double* c, double
         int tot = 0;
         for (int k = 0; k < S.ncomp - 1; k++) {
             sizes[k] = (int)ceil(S.p[k] * n);
+            if (sizes[k] > n - tot) sizes[k] = n - tot;  // oracle: or_cec_segments
             tot += sizes[k];
         }
         sizes[S.ncomp - 1] = n - tot;
@@ -327,6 +329,449 @@ __device__ inline double cec_eval_warp(const CecData& C, const double* c, double
         } else {
             for (int k = 0; k < S.ncomp; k++) wsum_ += w[k];
             for (int k = 0; k < S.ncomp; k++) f += w[k] / wsum_ * fit[k];
+        }
+    }
+    __syncwarp();
+    return f + S.fstar;
+}
+
+
+// ---------------------------------------------------------------------------
+// Batched evaluation: up to 8 candidates per warp, the rotation as one
+// [8 x n] x [n x n] contraction.
+//
+// DMMA path (n >= APO_CEC_DMMA_MIN_DIM): mma.sync m8n8k4 f64 on the tensor
+// cores.  A = Y (8 candidates x 4 input dims, shared memory), B = M^T
+// (4 input dims x 8 output dims, read through L1 from the transposed
+// rotation rot_t), C = Z (8 x 8).  Fragment layout (PTX ISA, m8n8k4 .f64):
+// lane = 4 g + t holds A[g][t], B[t][g] and C[g][2t], C[g][2t+1].  Two
+// n-tiles are in flight per k-step so consecutive mma's are independent.
+// FMA path (small n): lane j of the warp owns output dim j for all 8 rows,
+// so each loaded matrix element feeds 8 FMAs.
+#ifndef APO_CEC_DMMA_MIN_DIM
+#define APO_CEC_DMMA_MIN_DIM 16
+#endif
+
+__device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Z[q][j] = sum_i rot_t[i][j] * Y[q][i] + off, q < 8 (rows are independent:
+// rows past the batch hold stale but harmless values).
+__device__ inline void cec_rotate8(const double* __restrict__ rot_t, const double* Y, double* Z, int ys, int n,
+                                   double off, int lane) {
+    if (n >= APO_CEC_DMMA_MIN_DIM) {
+        const int g = lane >> 2, t = lane & 3;
+        const double* yrow = Y + (size_t)g * ys;
+        for (int j0 = 0; j0 < n; j0 += 16) {
+            const int ja = j0 + g, jb = j0 + 8 + g;
+            const bool va = ja < n, vb = jb < n;
+            double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+#pragma unroll 2
+            for (int i0 = 0; i0 < n; i0 += 4) {
+                const int i = i0 + t;
+                const bool vi = i < n;
+                const double a = vi ? yrow[i] : 0.0;
+                const double* brow = rot_t + (size_t)i * n;
+                const double b0 = (vi && va) ? __ldg(brow + ja) : 0.0;
+                const double b1 = (vi && vb) ? __ldg(brow + jb) : 0.0;
+                dmma_m8n8k4(c0, c1, a, b0);
+                dmma_m8n8k4(c2, c3, a, b1);
+            }
+            double* zrow = Z + (size_t)g * ys;
+            const int ca = j0 + 2 * t, cb = j0 + 8 + 2 * t;
+            if (ca < n) zrow[ca] = c0 + off;
+            if (ca + 1 < n) zrow[ca + 1] = c1 + off;
+            if (cb < n) zrow[cb] = c2 + off;
+            if (cb + 1 < n) zrow[cb + 1] = c3 + off;
+        }
+    } else {
+        for (int j = lane; j < n; j += 32) {
+            double acc[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) acc[q] = 0.0;
+            for (int i = 0; i < n; i++) {
+                const double m = __ldg(rot_t + (size_t)i * n + j);
+#pragma unroll
+                for (int q = 0; q < 8; q++) acc[q] = fma(m, Y[(size_t)q * ys + i], acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) Z[(size_t)q * ys + j] = acc[q] + off;
+        }
+    }
+}
+
+// F_fn for candidates X[q][0..n), q < nb (stride xs).  Z, W: scratch rows of
+// the same shape (W only for compositions).  X is overwritten.  Returns the
+// fitness of candidate q on lane q.
+__device__ inline double cec_eval_batch(const CecData& C, double* X, double* Z, double* W, int xs, int nb, int n,
+                                        int lane) {
+    const CecSpec& S = kCecSpec[C.fn - 1];
+    double mine = 0.0;
+    if (S.kind == 0) {
+        const int b = S.basic[0];
+        const double sc = cec_scale(b);
+        for (int q = 0; q < nb; q++) {
+            double* x = X + (size_t)q * xs;
+            for (int i = lane; i < n; i += 32) {
+                double xi = x[i];
+                const double oi = C.shift[i];
+                if (b == B_STEP_RASTRIGIN && fabs(xi - oi) > 0.5) xi = oi + floor(2.0 * (xi - oi) + 0.5) / 2.0;
+                x[i] = (xi - oi) * sc;
+            }
+        }
+        __syncwarp();
+        cec_rotate8(C.rot_t, X, Z, xs, n, cec_offset(b), lane);
+        __syncwarp();
+        for (int q = 0; q < nb; q++) {
+            const double v = cec_basic_warp(b, Z + (size_t)q * xs, n, lane);
+            if (lane == q) mine = v;
+        }
+    } else if (S.kind == 1) {
+        for (int q = 0; q < nb; q++) {
+            double* x = X + (size_t)q * xs;
+            for (int i = lane; i < n; i += 32) x[i] = x[i] - C.shift[i];
+        }
+        __syncwarp();
+        cec_rotate8(C.rot_t, X, Z, xs, n, 0.0, lane);
+        __syncwarp();
+        int sizes[6];
+        int tot = 0;
+        for (int k = 0; k < S.ncomp - 1; k++) {
+            sizes[k] = (int)ceil(S.p[k] * n);
+            if (sizes[k] > n - tot) sizes[k] = n - tot;  // oracle: or_cec_segments
+            tot += sizes[k];
+        }
+        sizes[S.ncomp - 1] = n - tot;
+        for (int q = 0; q < nb; q++) {
+            const double* z = Z + (size_t)q * xs;
+            double* y = X + (size_t)q * xs;
+            int start = 0;
+            for (int k = 0; k < S.ncomp; k++) {
+                const double sc = cec_scale(S.basic[k]), off = cec_offset(S.basic[k]);
+                for (int i = lane; i < sizes[k]; i += 32) y[start + i] = z[C.shuffle[start + i] - 1] * sc + off;
+                start += sizes[k];
+            }
+        }
+        __syncwarp();
+        for (int q = 0; q < nb; q++) {
+            const double* y = X + (size_t)q * xs;
+            double f = 0.0;
+            int start = 0;
+            for (int k = 0; k < S.ncomp; k++) {
+                if (sizes[k] > 0) f += cec_basic_warp(S.basic[k], y + start, sizes[k], lane);
+                start += sizes[k];
+            }
+            if (lane == q) mine = f;
+        }
+    } else {
+        double fit[6], w[6];
+        int inf_at = -1;
+        for (int k = 0; k < S.ncomp; k++) {
+            const int b = S.basic[k];
+            const double sc = cec_scale(b), off = cec_offset(b);
+            const double* o = C.shift + (size_t)k * n;
+            double d2_mine = 0.0;
+            for (int q = 0; q < nb; q++) {
+                const double* x = X + (size_t)q * xs;
+                double* y = W + (size_t)q * xs;
+                double* z = Z + (size_t)q * xs;
+                double d2 = 0.0;
+                for (int i = lane; i < n; i += 32) {
+                    const double dv = x[i] - o[i];
+                    d2 += dv * dv;
+                    y[i] = dv * sc;
+                    if (!S.rflag[k]) z[i] = dv * sc + off;
+                }
+                d2 = wsum(d2);
+                if (lane == q) d2_mine = d2;
+            }
+            __syncwarp();
+            if (S.rflag[k]) cec_rotate8(C.rot_t + (size_t)k * n * n, W, Z, xs, n, off, lane);
+            __syncwarp();
+            double fk = 0.0;
+            for (int q = 0; q < nb; q++) {
+                const double v = S.lam[k] * cec_basic_warp(b, Z + (size_t)q * xs, n, lane) + S.bias[k];
+                if (lane == q) fk = v;
+            }
+            __syncwarp();
+            fit[k] = fk;
+            w[k] = d2_mine != 0.0 ? sqrt(1.0 / d2_mine) * exp(-d2_mine / 2.0 / n / (S.sigma[k] * S.sigma[k]))
+                                  : __longlong_as_double(0x7ff0000000000000LL);
+            if (d2_mine == 0.0 && inf_at < 0) inf_at = k;
+        }
+        // combination (lane q holds candidate q's components)
+        double wmax = 0.0, wsum_ = 0.0, f = 0.0;
+        for (int k = 0; k < S.ncomp; k++)
+            if (w[k] > wmax) wmax = w[k];
+        if (inf_at >= 0) {
+            f = fit[inf_at];
+        } else if (wmax == 0.0) {
+            for (int k = 0; k < S.ncomp; k++) f += fit[k] / S.ncomp;
+        } else {
+            for (int k = 0; k < S.ncomp; k++) wsum_ += w[k];
+            for (int k = 0; k < S.ncomp; k++) f += w[k] / wsum_ * fit[k];
+        }
+        mine = f;
+    }
+    __syncwarp();
+    return mine + S.fstar;
+}
+
+
+// ---------------------------------------------------------------------------
+// k_cec_eval's evaluator: 8 candidates per warp, one QUAD of lanes per
+// candidate (lane = 4 q + t).  This is the DMMA m8n8k4 fragment layout (A
+// row g = lane/4, column t = lane%4), so the same quad that owns row q of the
+// rotation input also evaluates candidate q: elements i = t, t+4, ... and two
+// shuffles reduce a quad.  Rows are zero-padded to n4 = round_up(n, 4) and
+// the rotation reads a zero-padded copy of M^T (rot_pad: [n4][8 NT] per
+// component), so the inner loop carries no bounds checks.
+__device__ __forceinline__ double qsum(double v) {
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+    v += __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+    return v;
+}
+__device__ __forceinline__ double qprod(double v) {
+    v *= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+    v *= __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+    return v;
+}
+
+// Y[q][:] <- M Y[q][:] + off for the 8 rows of the warp, in place: all
+// output tiles accumulate in registers (n <= 8 NT), A from shared memory,
+// B through L1 from rot_pad.
+template <int NT>
+__device__ __forceinline__ void cec_rotate_quad(const double* __restrict__ rot_pad, double* Y, int ys, int n,
+                                                double off, int lane) {
+    const int g = lane >> 2, t = lane & 3;
+    const int n4 = (n + 3) & ~3;
+    double acc[NT][2];
+#pragma unroll
+    for (int k = 0; k < NT; k++) acc[k][0] = acc[k][1] = 0.0;
+    double* yrow = Y + (size_t)g * ys;
+    const double* bp = rot_pad + (size_t)t * (8 * NT) + g;
+#pragma unroll 2
+    for (int i0 = 0; i0 < n4; i0 += 4) {
+        const double a = yrow[i0 + t];
+        double b[NT];
+#pragma unroll
+        for (int k = 0; k < NT; k++) b[k] = __ldg(bp + 8 * k);
+#pragma unroll
+        for (int k = 0; k < NT; k++) dmma_m8n8k4(acc[k][0], acc[k][1], a, b[k]);
+        bp += 4 * (8 * NT);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NT; k++) {
+        const int c = 8 * k + 2 * t;
+        if (c < n) yrow[c] = acc[k][0] + off;
+        if (c + 1 < n) yrow[c + 1] = acc[k][1] + off;
+    }
+    __syncwarp();
+}
+
+// Basic function b over z[0..n) by the 4 lanes of a quad; every lane of the
+// quad returns the value.  ew: host-computed ELLIPS weights (nullable).
+__device__ inline double cec_basic_quad(int b, const double* z, int n, int t, const double* ew) {
+    double a = 0.0, c = 0.0;
+    switch (b) {
+    case B_ZAKHAROV:
+        for (int i = t; i < n; i += 4) {
+            a += z[i] * z[i];
+            c += 0.5 * (i + 1) * z[i];
+        }
+        a = qsum(a);
+        c = qsum(c);
+        return a + c * c + c * c * c * c;
+    case B_ROSENBROCK:
+        for (int i = t; i < n - 1; i += 4) {
+            const double t1 = z[i] * z[i] - z[i + 1], t2 = z[i] - 1.0;
+            a += 100.0 * t1 * t1 + t2 * t2;
+        }
+        return qsum(a);
+    case B_ESCAFFER6:
+        for (int i = t; i < n; i += 4) a += schaffer_g(z[i], z[i + 1 < n ? i + 1 : 0]);
+        return qsum(a);
+    case B_RASTRIGIN:
+    case B_STEP_RASTRIGIN:
+        for (int i = t; i < n; i += 4) a += z[i] * z[i] - 10.0 * cospi(2.0 * z[i]) + 10.0;
+        return qsum(a);
+    case B_LEVY: {
+        for (int i = t; i < n - 1; i += 4) {
+            const double wi = 1.0 + z[i] / 4.0;
+            const double s = sin(kPi * wi + 1.0);
+            a += (wi - 1.0) * (wi - 1.0) * (1.0 + 10.0 * s * s);
+        }
+        a = qsum(a);
+        const double w0 = 1.0 + z[0] / 4.0, wn = 1.0 + z[n - 1] / 4.0;
+        const double s0 = sin(kPi * w0), sn = sin(2.0 * kPi * wn);
+        return s0 * s0 + a + (wn - 1.0) * (wn - 1.0) * (1.0 + sn * sn);
+    }
+    case B_BENT_CIGAR:
+        for (int i = t; i < n; i += 4)
+            if (i >= 1) a += z[i] * z[i];
+        return z[0] * z[0] + 1e6 * qsum(a);
+    case B_DISCUS:
+        for (int i = t; i < n; i += 4)
+            if (i >= 1) a += z[i] * z[i];
+        return 1e6 * z[0] * z[0] + qsum(a);
+    case B_ELLIPS:
+        for (int i = t; i < n; i += 4)
+            a += (ew ? ew[i] : pow(10.0, 6.0 * i / (n > 1 ? n - 1 : 1))) * z[i] * z[i];
+        return qsum(a);
+    case B_HGBAT:
+    case B_HAPPYCAT: {
+        for (int i = t; i < n; i += 4) {
+            a += z[i] * z[i];
+            c += z[i];
+        }
+        a = qsum(a);
+        c = qsum(c);
+        if (b == B_HGBAT) return sqrt(fabs(a * a - c * c)) + (0.5 * a + c) / n + 0.5;
+        return pow(fabs(a - n), 0.25) + (0.5 * a + c) / n + 0.5;
+    }
+    case B_KATSUURA: {
+        const double t3 = pow((double)n, 1.2);
+        double pr = 1.0;
+        for (int i = t; i < n; i += 4) {
+            double s = 0.0;
+            double t1 = 1.0, inv = 1.0;
+#pragma unroll 8
+            for (int j = 1; j <= 32; j++) {
+                t1 *= 2.0;  // 2^j and 2^-j are exact
+                inv *= 0.5;
+                const double t2 = t1 * z[i];
+                s += fabs(t2 - floor(t2 + 0.5)) * inv;
+            }
+            pr *= pow(1.0 + (i + 1) * s, 10.0 / t3);
+        }
+        pr = qprod(pr);
+        const double t1 = 10.0 / n / n;
+        return pr * t1 - t1;
+    }
+    case B_ACKLEY: {
+        for (int i = t; i < n; i += 4) {
+            a += z[i] * z[i];
+            c += cospi(2.0 * z[i]);
+        }
+        a = qsum(a);
+        c = qsum(c);
+        return kE - 20.0 * exp(-0.2 * sqrt(a / n)) - exp(c / n) + 20.0;
+    }
+    case B_SCHWEFEL:
+        for (int i = t; i < n; i += 4) a += schwefel_t(z[i] + 4.209687462275036e+002, n);
+        return qsum(a) + 4.189828872724338e+002 * n;
+    case B_SCHAFFER_F7: {
+        for (int i = t; i < n - 1; i += 4) {
+            const double zi = sqrt(z[i] * z[i] + z[i + 1] * z[i + 1]);
+            const double s = sin(50.0 * pow(zi, 0.2));
+            a += sqrt(zi) + sqrt(zi) * s * s;
+        }
+        a = qsum(a);
+        return n > 1 ? a * a / (n - 1) / (n - 1) : a * a;
+    }
+    case B_GRIE_ROSEN:
+        for (int i = t; i < n; i += 4) a += grie_rosen_t(z[i], z[i + 1 < n ? i + 1 : 0]);
+        return qsum(a);
+    default: {  // B_GRIEWANK
+        double pr = 1.0;
+        for (int i = t; i < n; i += 4) {
+            a += z[i] * z[i];
+            pr *= cos(z[i] / sqrt(1.0 + i));
+        }
+        return 1.0 + qsum(a) / 4000.0 - qprod(pr);
+    }
+    }
+}
+
+// F_fn of the warp's 8 rows X[q] (stride xs, zero-padded to n4); W: second
+// row buffer (hybrids, compositions).  X is overwritten except for
+// compositions.  Every lane of quad q returns candidate q's fitness.
+template <int NT>
+__device__ inline double cec_eval_quad(const CecData& C, double* X, double* W, int xs, int n, int lane,
+                                       const double* ew) {
+    const CecSpec& S = kCecSpec[C.fn - 1];
+    const int q = lane >> 2, t = lane & 3;
+    const int n4 = (n + 3) & ~3;
+    double* x = X + (size_t)q * xs;
+    double* w = W + (size_t)q * xs;
+    double f = 0.0;
+    if (S.kind == 0) {
+        const int b = S.basic[0];
+        const double sc = cec_scale(b);
+        for (int i = t; i < n; i += 4) {
+            double xi = x[i];
+            const double oi = C.shift[i];
+            if (b == B_STEP_RASTRIGIN && fabs(xi - oi) > 0.5) xi = oi + floor(2.0 * (xi - oi) + 0.5) / 2.0;
+            x[i] = (xi - oi) * sc;
+        }
+        __syncwarp();
+        cec_rotate_quad<NT>(C.rot_pad, X, xs, n, cec_offset(b), lane);
+        f = cec_basic_quad(b, x, n, t, ew);
+    } else if (S.kind == 1) {
+        for (int i = t; i < n; i += 4) x[i] = x[i] - C.shift[i];
+        __syncwarp();
+        cec_rotate_quad<NT>(C.rot_pad, X, xs, n, 0.0, lane);
+        int sizes[6];
+        int tot = 0;
+        for (int k = 0; k < S.ncomp - 1; k++) {
+            sizes[k] = (int)ceil(S.p[k] * n);
+            if (sizes[k] > n - tot) sizes[k] = n - tot;  // oracle: or_cec_segments
+            tot += sizes[k];
+        }
+        sizes[S.ncomp - 1] = n - tot;
+        int start = 0;
+        for (int k = 0; k < S.ncomp; k++) {
+            const double sc = cec_scale(S.basic[k]), off = cec_offset(S.basic[k]);
+            for (int i = t; i < sizes[k]; i += 4) w[start + i] = x[C.shuffle[start + i] - 1] * sc + off;
+            start += sizes[k];
+        }
+        __syncwarp();
+        start = 0;
+        for (int k = 0; k < S.ncomp; k++) {
+            if (sizes[k] > 0) f += cec_basic_quad(S.basic[k], w + start, sizes[k], t, ew);
+            start += sizes[k];
+        }
+    } else {
+        double fit[6], wk[6];
+        int inf_at = -1;
+        for (int k = 0; k < S.ncomp; k++) {
+            const int b = S.basic[k];
+            const double sc = cec_scale(b), off = cec_offset(b);
+            const double* o = C.shift + (size_t)k * n;
+            const bool rot = S.rflag[k] != 0;
+            double d2 = 0.0;
+            for (int i = t; i < n4; i += 4) {
+                if (i < n) {
+                    const double dv = x[i] - o[i];
+                    d2 += dv * dv;
+                    w[i] = rot ? dv * sc : dv * sc + off;
+                } else {
+                    w[i] = 0.0;
+                }
+            }
+            d2 = qsum(d2);
+            __syncwarp();
+            if (rot) cec_rotate_quad<NT>(C.rot_pad + (size_t)k * n4 * (8 * NT), W, xs, n, off, lane);
+            fit[k] = S.lam[k] * cec_basic_quad(b, w, n, t, ew) + S.bias[k];
+            __syncwarp();
+            wk[k] = d2 != 0.0 ? sqrt(1.0 / d2) * exp(-d2 / 2.0 / n / (S.sigma[k] * S.sigma[k]))
+                              : __longlong_as_double(0x7ff0000000000000LL);
+            if (d2 == 0.0 && inf_at < 0) inf_at = k;
+        }
+        double wmax = 0.0, wsum_ = 0.0;
+        for (int k = 0; k < S.ncomp; k++)
+            if (wk[k] > wmax) wmax = wk[k];
+        if (inf_at >= 0) {
+            f = fit[inf_at];
+        } else if (wmax == 0.0) {
+            for (int k = 0; k < S.ncomp; k++) f += fit[k] / S.ncomp;
+        } else {
+            for (int k = 0; k < S.ncomp; k++) wsum_ += wk[k];
+            for (int k = 0; k < S.ncomp; k++) f += wk[k] / wsum_ * fit[k];
         }
     }
     __syncwarp();

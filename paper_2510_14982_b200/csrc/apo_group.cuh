@@ -89,7 +89,7 @@ struct GroupScratch {
     double* ring;         // [kStages][4][rld] staged rows (nullptr if not staging)
     uint64_t* bar;        // [kStages] mbarriers of the ring
     WarpScratch ws;       // only ws.pk / ws.pw (pair cache for npairs > 1) are used
-    int dp, words, tstride, batch, rld;
+    int dp, words, tstride, cstride, batch, rld;
 };
 
 __host__ __device__ inline int ring_ld(int dim) { return (dim + 1) & ~1; }
@@ -107,21 +107,39 @@ __host__ __device__ inline size_t group_head_bytes(int dim) {
     return (b + 15) & ~(size_t)15;
 }
 
-__host__ __device__ inline size_t group_union_bytes(int dim) {
+// CEC2022 objectives evaluate kCecRows candidates at once (one DMMA m-tile):
+// rows X (candidates), Z (rotation output) and, for compositions, W (the
+// per-component shifted copy), each kCecRows x cec_stride doubles.  The
+// stride is a multiple of 4 that is not a multiple of 8, so the A-fragment
+// loads of a DMMA (rows g = lane/4, columns t = lane%4) are bank-conflict
+// free.  cec_bufs = 0 (not CEC), 2 (F1-F8) or 3 (F9-F12).
+constexpr int kCecRows = 8;
+__host__ __device__ inline int cec_stride(int dim) {
+    const int s = (dim + 3) & ~3;
+    return (s & 7) ? s : s + 4;
+}
+__host__ __device__ inline int cec_bufs_for(int code) {
+    return code <= 100 ? 0 : (code - 100 >= 9 ? 3 : 2);
+}
+
+__host__ __device__ inline size_t group_union_bytes(int dim, int cec_bufs = 0) {
     const size_t perm = 32 * (size_t)((dim + 3) & ~3);
-    const size_t terms = 8 * (size_t)group_batch(dim) * (size_t)group_tstride(dim);
+    size_t terms = 8 * (size_t)group_batch(dim) * (size_t)group_tstride(dim);
+    const size_t cec = 8 * (size_t)cec_bufs * kCecRows * (size_t)cec_stride(dim);
+    if (cec > terms) terms = cec;
     return ((perm > terms ? perm : terms) + 15) / 16 * 16;
 }
 
-__host__ __device__ inline size_t group_scratch_bytes(int dim, bool stage = false) {
-    return group_head_bytes(dim) + group_union_bytes(dim) + ring_bytes(dim, stage);
+__host__ __device__ inline size_t group_scratch_bytes(int dim, bool stage = false, int cec_bufs = 0) {
+    return group_head_bytes(dim) + group_union_bytes(dim, cec_bufs) + ring_bytes(dim, stage);
 }
 
-__device__ inline GroupScratch group_scratch(unsigned char* base, int dim, bool stage = false) {
+__device__ inline GroupScratch group_scratch(unsigned char* base, int dim, bool stage = false, int cec_bufs = 0) {
     GroupScratch g;
     g.dp = (dim + 3) & ~3;
     g.words = (dim + 31) / 32;
     g.tstride = group_tstride(dim);
+    g.cstride = cec_stride(dim);
     g.batch = group_batch(dim);
     g.f = reinterpret_cast<double*>(base);
     g.sgn = g.f + 32;
@@ -135,7 +153,7 @@ __device__ inline GroupScratch group_scratch(unsigned char* base, int dim, bool 
     g.T = reinterpret_cast<double*>(base + group_head_bytes(dim));
     g.rld = ring_ld(dim);
     if (stage) {
-        g.ring = reinterpret_cast<double*>(base + group_head_bytes(dim) + group_union_bytes(dim));
+        g.ring = reinterpret_cast<double*>(base + group_head_bytes(dim) + group_union_bytes(dim, cec_bufs));
         g.bar = reinterpret_cast<uint64_t*>(g.ring + (size_t)kStages * 4 * g.rld);
     } else {
         g.ring = nullptr;
@@ -373,9 +391,9 @@ __device__ __forceinline__ double clampv(double c, double lo, double hi) {
 }
 
 // hgbat/griewank stage two term rows per protozoon; CEC objectives stage the
-// candidate itself and use the second half as rotation scratch.
+// candidate itself (rows of stride cstride, see cec_stride).
 __device__ __forceinline__ bool two_term_arrays(int code) {
-    return code == OBJ_HGBAT || code == OBJ_GRIEWANK || code >= OBJ_CEC_BASE;
+    return code == OBJ_HGBAT || code == OBJ_GRIEWANK;
 }
 
 // Per-dimension fitness terms of candidate value c at dimension d (c_prev =
@@ -577,7 +595,8 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
                                     const uint8_t* in_dr_bytes, const unsigned* in_dr_bits, const double* p_dr,
                                     double* out_rows, double* out_fit, bool out_by_slot, uint8_t* out_acc,
                                     uint8_t* out_warn, uint8_t* sel_next, const GroupScratch& g, int lane,
-                                    unsigned long long& my_min, unsigned& my_warn, unsigned* ring_phase = nullptr) {
+                                    unsigned long long& my_min, unsigned& my_warn, unsigned* ring_phase = nullptr,
+                                    uint8_t* cand_ok = nullptr) {
     if (lane < n) {
         const int r0 = i0 - 1 + lane;
         const bool dr = in_dr_bits ? ((in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0 : in_dr_bytes[r0] != 0;
@@ -608,7 +627,12 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
         for (int p = 0; p < kStages && p < n; p++) issue(p);
     }
     const bool two = two_term_arrays(O.code);
-    const int B = two ? g.batch / 2 : g.batch;
+    const bool cec = O.code >= OBJ_CEC_BASE;
+    const int ts = cec ? g.cstride : g.tstride;
+    // cand_ok != nullptr: candidates only (written + finiteness flag); the
+    // fitness, greedy select and best-so-far run in k_cec_eval (CEC2022 on HBM).
+    const bool cand_only = cand_ok != nullptr;
+    const int B = cand_only ? 32 : cec ? kCecRows : two ? g.batch / 2 : g.batch;
     double* T2base = g.T + (size_t)(g.batch / 2) * g.tstride;
     for (int h = 0; h < n; h += B) {
         const int nb = min(B, n - h);
@@ -619,7 +643,7 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
             double* dst;
             if constexpr (MODE == OUT_SEL) dst = R.alt_key(own_key);
             else dst = out_rows + (size_t)(out_by_slot ? R.slot_of(own_key) : i - 1) * P.ld;
-            double* T1 = g.T + (size_t)q * g.tstride;
+            double* T1 = cand_only ? g.T : g.T + (size_t)q * ts;
             double* T2 = two ? T2base + (size_t)q * g.tstride : nullptr;
             const double* staged = nullptr;
             if (staging) {
@@ -638,16 +662,19 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
             }
         }
         __syncwarp();
+        if (cand_only) {
+            if (lane < nb) {
+                const int own_key = g.slot[4 * (h + lane)];
+                cand_ok[MODE == OUT_SEL ? R.slot_of(own_key) : i0 - 1 + h + lane] = (uint8_t)((okmask >> lane) & 1u);
+            }
+            __syncwarp();
+            continue;
+        }
         bool acc = false, warned = false;
         double cec_f = 0.0;
-        if (O.code >= OBJ_CEC_BASE) {  // warp-cooperative evaluation of each staged candidate
-            for (int q = 0; q < nb; q++) {
-                if (!((okmask >> q) & 1u)) continue;
-                const double fq = cec_eval_warp(O.cec, g.T + (size_t)q * g.tstride, T2base, T2base + g.tstride,
-                                                P.dim, lane);
-                if (lane == q) cec_f = fq;
-            }
-        }
+        if (cec)  // the batch's staged candidates together (DMMA rotation, apo_cec.cuh)
+            cec_f = cec_eval_batch(O.cec, g.T, g.T + (size_t)kCecRows * ts, g.T + (size_t)2 * kCecRows * ts, ts, nb,
+                                   P.dim, lane);
         if (lane < nb) {
             const int p = h + lane, i = i0 + p;
             const int own_key = g.slot[4 * p];

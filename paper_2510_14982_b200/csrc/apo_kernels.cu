@@ -86,6 +86,7 @@ ObjDesc to_desc(const apo_objective* o) {
     d.cec.shift = o->shift;
     d.cec.rot_t = o->rot_t;
     d.cec.shuffle = o->shuffle;
+    d.cec.rot_pad = o->rot_pad;
     return d;
 }
 
@@ -258,24 +259,70 @@ __global__ void k_debug_exp(const double* x, double* out, long long n) {
 
 
 
-int launch_update(bool sel_mode, const UpdArgs& A, cudaStream_t st) {
-    const int dim = A.P.dim;
+// Fused update launch.  CEC2022 objectives with dim <= kCecEvalMaxDim and a
+// cand_ok scratch run as two kernels: k_update_group writes the candidates,
+// k_cec_eval evaluates them in DMMA tiles and finishes the update.
+// mid_event (nullable) is recorded between the two.
+int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* cand_ok = nullptr,
+                  cudaEvent_t mid_event = nullptr) {
+    UpdArgs a = A0;
+    const int dim = a.P.dim;
     const bool group = dim <= kGroupMaxDim;
+    const bool split = group && cand_ok && a.O.code > APO_OBJ_CEC2022_BASE && dim <= kCecEvalMaxDim &&
+                       a.O.cec.rot_pad != nullptr;
+    if (split) {
+        a.cand_ok = cand_ok;
+        a.cec_bufs = 0;
+    }
     const int w = group ? kWarps : warps_for_dim(dim);
     const bool stage = sel_mode && dim <= APO_STAGE_MAX_DIM;
-    const size_t smem = (group ? group_scratch_bytes(dim, stage) : warp_scratch_bytes(dim)) * (size_t)w;
+    const size_t smem = (group ? group_scratch_bytes(dim, stage, a.cec_bufs) : warp_scratch_bytes(dim)) * (size_t)w;
     const void* fn = sel_mode ? pick_update_sel(dim) : pick_update_dense(dim);
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
     if (per_sm < 1) per_sm = 1;
-    const long long units = group ? ((long long)A.P.ps + 31) / 32 : (long long)A.P.ps;
+    const long long units = group ? ((long long)a.P.ps + 31) / 32 : (long long)a.P.ps;
     const long long need = (units + w - 1) / w;
     const long long cap = (long long)per_sm * num_sms();
     const int grid = (int)(need < cap ? need : cap);
-    UpdArgs a = A;
-    void* args[] = {(void*)&a};
-    APO_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(32 * w), args, smem, st));
+    {
+        void* args[] = {(void*)&a};
+        APO_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(32 * w), args, smem, st));
+    }
+    if (mid_event) APO_CUDA(cudaEventRecord(mid_event, st));
+    if (!split) return APO_OK;
+    CecEvalArgs E{};
+    E.n_rows = a.P.ps;
+    E.dim = dim;
+    E.ld = a.P.ld;
+    E.O = a.O;
+    const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
+    E.bufs = (fn_id >= 6) ? 2 : 1;
+    E.pos0 = a.pos0;
+    E.pos1 = a.pos1;
+    E.sel = a.sel;
+    E.sel_next = a.sel_next;
+    E.pos = a.pos;
+    E.out_pos = a.out_pos;
+    E.out_acc = a.out_acc;
+    E.out_warn = a.out_warn;
+    E.fit = a.fit;
+    E.out_fit = a.out_fit;
+    E.cand_ok = cand_ok;
+    E.warn_count = a.warn_count;
+    E.trace_key = a.trace_key;
+    const void* fe = pick_cec_eval(sel_mode, dim);
+    const size_t esmem = cec_eval_warp_bytes(dim, E.bufs) * kWarps;
+    if (int rc = set_smem(fe, esmem)) return rc;
+    int eper = 1;
+    APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&eper, fe, kThreads, esmem));
+    if (eper < 1) eper = 1;
+    const long long tiles = ((long long)E.n_rows + kCecRows - 1) / kCecRows;
+    const long long eneed = (tiles + kWarps - 1) / kWarps;
+    const long long ecap = (long long)eper * num_sms();
+    void* eargs[] = {(void*)&E};
+    APO_CUDA(cudaLaunchKernel(fe, dim3((unsigned)(eneed < ecap ? eneed : ecap)), dim3(kThreads), eargs, esmem, st));
     return APO_OK;
 }
 
@@ -351,6 +398,7 @@ struct apo_run {
     void* tmp;
     size_t tmp_bytes;
     double* p_dr;
+    uint8_t* cand_ok;  // CEC2022 split update: per-slot candidate finiteness
     std::vector<double> sched;
     unsigned long long* trace_keys;  // [T+1]
     unsigned long long* warn;
@@ -411,7 +459,13 @@ int apo_run_updates_obj(const double* positions, const double* fitness, const ui
     A.out_acc = out_acc;
     A.out_warn = out_warn;
     A.warn_count = warn_count;
-    return launch_update(false, A, as_stream(stream));
+    A.cec_bufs = cec_bufs_for(A.O.code);
+    uint8_t* cand_ok = nullptr;
+    const bool cec = A.O.code > APO_OBJ_CEC2022_BASE;
+    if (cec) APO_CUDA(cudaMallocAsync((void**)&cand_ok, (size_t)ps, as_stream(stream)));
+    const int rc = launch_update(false, A, as_stream(stream), cand_ok);
+    if (cec) cudaFreeAsync(cand_ok, as_stream(stream));
+    return rc;
 }
 
 int apo_run_updates(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
@@ -586,6 +640,7 @@ int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iteration
     alloc((void**)&r->dr_bits, 4 * (size_t)((ps + 31) / 32));
     alloc(&r->tmp, r->tmp_bytes);
     alloc((void**)&r->p_dr, 8 * (size_t)ps);
+    alloc((void**)&r->cand_ok, (size_t)ps);
     alloc((void**)&r->trace_keys, 8 * (size_t)(max_iterations + 1));
     alloc((void**)&r->warn, 8);
     if (e != cudaSuccess) {
@@ -658,7 +713,7 @@ int apo_run_iterate(apo_run* r, int64_t n) {
         P.p_ah = r->sched[3 * t];
         P.f_mult = r->sched[3 * t + 1];
         P.decay = r->sched[3 * t + 2];
-        cudaEvent_t ev[2] = {nullptr, nullptr};
+        cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
         if (r->profile) {
             for (auto& e : ev) {
                 APO_CUDA(cudaEventCreate(&e));
@@ -680,8 +735,9 @@ int apo_run_iterate(apo_run* r, int64_t n) {
         A.p_dr = r->p_dr;
         A.warn_count = r->warn;
         A.trace_key = r->trace_keys + t + 1;
-        if (int rc = launch_update(true, A, st)) return rc;
-        if (r->profile) APO_CUDA(cudaEventRecord(ev[1], st));
+        A.cec_bufs = cec_bufs_for(r->obj.code);
+        if (int rc = launch_update(true, A, st, r->cand_ok, ev[1])) return rc;
+        if (r->profile) APO_CUDA(cudaEventRecord(ev[2], st));
         r->cur ^= 1;
         r->iters++;
     }
@@ -770,17 +826,27 @@ int apo_run_profile(apo_run* r, int enable) {
     return APO_OK;
 }
 
-int apo_run_profile_read(apo_run* r, double* update_ms_host, int64_t* launches_host) {
+int apo_run_profile_split(apo_run* r, double* candidates_ms_host, double* evaluate_ms_host, int64_t* launches_host) {
     APO_CHECK(r, "run is NULL");
     APO_CUDA(cudaStreamSynchronize(r->stream));
-    double total = 0.0;
-    for (size_t k = 0; k + 1 < r->prof_events.size(); k += 2) {
-        float ms = 0.f;
-        APO_CUDA(cudaEventElapsedTime(&ms, r->prof_events[k], r->prof_events[k + 1]));
-        total += ms;
+    double a = 0.0, b = 0.0;
+    for (size_t k = 0; k + 2 < r->prof_events.size(); k += 3) {
+        float m1 = 0.f, m2 = 0.f;
+        APO_CUDA(cudaEventElapsedTime(&m1, r->prof_events[k], r->prof_events[k + 1]));
+        APO_CUDA(cudaEventElapsedTime(&m2, r->prof_events[k + 1], r->prof_events[k + 2]));
+        a += m1;
+        b += m2;
     }
-    if (update_ms_host) *update_ms_host = total;
-    if (launches_host) *launches_host = (int64_t)(r->prof_events.size() / 2);
+    if (candidates_ms_host) *candidates_ms_host = a;
+    if (evaluate_ms_host) *evaluate_ms_host = b;
+    if (launches_host) *launches_host = (int64_t)(r->prof_events.size() / 3);
+    return APO_OK;
+}
+
+int apo_run_profile_read(apo_run* r, double* update_ms_host, int64_t* launches_host) {
+    double a = 0.0, b = 0.0;
+    if (int rc = apo_run_profile_split(r, &a, &b, launches_host)) return rc;
+    if (update_ms_host) *update_ms_host = a + b;
     return APO_OK;
 }
 
@@ -788,7 +854,7 @@ int apo_run_destroy(apo_run* r) {
     if (!r) return APO_OK;
     clear_profile(r);
     void* bufs[] = {r->pos[0], r->pos[1], r->sel[0], r->sel[1], r->fit[0], r->fit[1], r->order, r->keys_in, r->keys_out, r->vals_in,
-                    r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn};
+                    r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn, r->cand_ok};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete r;
@@ -802,7 +868,7 @@ int64_t apo_run_batch_max_elems(int64_t ps, int64_t dim) {
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
     const int64_t ld = (dim + 1) & ~1LL;
-    const BatchLayout L = batch_layout((int)ps, (int)dim, (int)ld, kWarps);
+    const BatchLayout L = batch_layout((int)ps, (int)dim, (int)ld, kWarps, 0);
     return (int64_t)L.total + 2048 <= optin ? ps * dim : 0;
 }
 
@@ -847,7 +913,18 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     A.final_pos = final_pos;
     A.final_fit = final_fit;
     A.warnings = (long long*)warnings;
-    const BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps);
+    A.cec_bufs = 0;
+    for (int64_t k = 0; k < nruns; k++) {
+        const int cb = cec_bufs_for(objectives_host[k].code);
+        if (cb > A.cec_bufs) A.cec_bufs = cb;
+    }
+    const BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs);
+    {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
+        APO_CHECK((int64_t)L.total + 2048 <= optin, "population too large for the shared-memory batch kernel");
+    }
     const void* fn = pick_run_batch((int)dim);
     if (int rc = set_smem(fn, L.total)) return rc;
     void* args[] = {(void*)&A};

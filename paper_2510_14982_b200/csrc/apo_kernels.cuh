@@ -39,6 +39,8 @@ struct UpdArgs {
     uint8_t* out_warn;
     unsigned long long* warn_count;
     unsigned long long* trace_key;
+    int cec_bufs;      // CEC2022 scratch rows (cec_bufs_for(code))
+    uint8_t* cand_ok;  // non-null: candidates only (k_cec_eval finishes the update)
 };
 
 __device__ __forceinline__ void block_finish(unsigned long long my_min, unsigned my_warn,
@@ -118,8 +120,8 @@ __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     // SEL rows have an even stride (16-byte aligned) -> TMA-staged rows
     constexpr bool kStage = SEL && MAXC > 0 && 32 * MAXC <= APO_STAGE_MAX_DIM;
-    const GroupScratch g =
-        group_scratch(smem + (size_t)warp * group_scratch_bytes(P.dim, kStage), P.dim, kStage);
+    const GroupScratch g = group_scratch(smem + (size_t)warp * group_scratch_bytes(P.dim, kStage, A.cec_bufs), P.dim,
+                                         kStage, A.cec_bufs);
     unsigned ring_phase = 0;
     if (kStage) {
         if (lane < kStages) mbar_init(&g.bar[lane], 1);
@@ -135,12 +137,13 @@ __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group
         if constexpr (SEL) {
             const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
             update_group<MAXC, OUT_SEL>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
-                                        true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn, &ring_phase);
+                                        true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn, &ring_phase,
+                                        A.cand_ok);
         } else {
             const DenseSlots R{A.pos, A.fit, P.ld};
             update_group<MAXC, OUT_FIXUP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
                                           A.out_fit, false, A.out_acc, A.out_warn, nullptr, g, lane, my_min,
-                                          my_warn);
+                                          my_warn, nullptr, A.cand_ok);
         }
     }
     block_finish(my_min, my_warn, A.warn_count, A.trace_key);
@@ -161,20 +164,21 @@ struct BatchArgs {
     double* final_pos;
     double* final_fit;
     long long* warnings;
+    int cec_bufs;  // max over the batch's objectives of cec_bufs_for(code)
 };
 
 struct BatchLayout {
     size_t pos0, pos1, fit0, fit1, keys, order, rankof, newrank, chead, cprev, crj, cbits, warps, total;
 };
 
-__host__ __device__ inline size_t batch_warp_bytes(int dim) {
+__host__ __device__ inline size_t batch_warp_bytes(int dim, int cec_bufs) {
     const size_t ws = warp_scratch_bytes(dim);  // init + warp path
     if (dim > kGroupMaxDim) return ws;
-    const size_t gs = group_scratch_bytes(dim);
+    const size_t gs = group_scratch_bytes(dim, false, cec_bufs);
     return gs > ws ? gs : ws;
 }
 
-__host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int nwarps) {
+__host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int nwarps, int cec_bufs) {
     BatchLayout L;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -194,7 +198,7 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
     L.cprev = take(4 * (size_t)ps);
     L.crj = take(4 * (size_t)ps);
     L.cbits = take(4 * (size_t)((ps + 31) / 32));
-    L.warps = take(batch_warp_bytes(dim) * (size_t)nwarps);
+    L.warps = take(batch_warp_bytes(dim, cec_bufs) * (size_t)nwarps);
     L.total = o;
     return L;
 }
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int run = blockIdx.x;
     const int ps = A.ps, dim = A.dim, ld = A.ld;
-    const BatchLayout L = batch_layout(ps, dim, ld, nwarps);
+    const BatchLayout L = batch_layout(ps, dim, ld, nwarps, A.cec_bufs);
     double* pos[2] = {reinterpret_cast<double*>(smem + L.pos0), reinterpret_cast<double*>(smem + L.pos1)};
     double* fit[2] = {reinterpret_cast<double*>(smem + L.fit0), reinterpret_cast<double*>(smem + L.fit1)};
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + L.keys);
@@ -221,8 +225,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
     cs.prev = reinterpret_cast<int*>(smem + L.cprev);
     cs.rj = reinterpret_cast<int*>(smem + L.crj);
     cs.bits = reinterpret_cast<unsigned*>(smem + L.cbits);
-    unsigned char* wbase = smem + L.warps + (size_t)warp * batch_warp_bytes(dim);
-    const GroupScratch g = group_scratch(wbase, dim);
+    unsigned char* wbase = smem + L.warps + (size_t)warp * batch_warp_bytes(dim, A.cec_bufs);
+    const GroupScratch g = group_scratch(wbase, dim, false, A.cec_bufs);
     const WarpScratch ws = MAXC >= 0 ? g.ws : warp_scratch(wbase, dim);
     const uint64_t seed = A.seeds[run];
     const ObjDesc O = A.objs[run];
@@ -369,9 +373,113 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
         for (int r = threadIdx.x; r < ps; r += blockDim.x) A.final_fit[(size_t)run * ps + r] = fit[cur][order[r]];
 }
 
+
+// ---------------------------------------------------------------------------
+// CEC2022 on an HBM-resident population: k_update_group writes every
+// candidate (+ a finiteness flag) and k_cec_eval then evaluates them in
+// 8-row DMMA tiles (one tile per warp), applies the greedy select
+// (numba_backend.py:270-290) and folds the best-so-far / warning count.
+// Rows are indexed by slot (SEL: the candidate is in the slot's alternate
+// buffer) or by rank (dense: the candidate is out_pos[r]; rejected rows are
+// rewritten with the old row).
+constexpr int kCecEvalMaxDim = 104;  // 13 register-resident n-tiles
+// n-tiles per rotation in k_cec_eval (rot_pad rows are 8 * cec_nt(n) wide)
+__host__ __device__ inline int cec_nt(int n) { return n <= 16 ? 2 : n <= 32 ? 4 : n <= 56 ? 7 : 13; }
+struct CecEvalArgs {
+    int n_rows, dim, ld, bufs;
+    ObjDesc O;
+    const double* pos0;  // SEL
+    const double* pos1;
+    const uint8_t* sel;
+    uint8_t* sel_next;
+    const double* pos;  // dense: old rows (rank order)
+    double* out_pos;    // dense: candidates in, kept rows out
+    uint8_t* out_acc;
+    uint8_t* out_warn;
+    const double* fit;
+    double* out_fit;
+    const uint8_t* cand_ok;
+    unsigned long long* warn_count;
+    unsigned long long* trace_key;
+};
+
+__host__ __device__ inline size_t cec_eval_warp_bytes(int dim, int bufs) {
+    return 8 * (size_t)bufs * kCecRows * (size_t)cec_stride(dim);
+}
+
+template <bool SEL, int NT>
+__global__ void __launch_bounds__(kThreads, 2) k_cec_eval(CecEvalArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int q = lane >> 2, t = lane & 3;  // quad q owns row q of the tile
+    const int dim = A.dim, cs = cec_stride(dim), n4 = (dim + 3) & ~3;
+    double* X = reinterpret_cast<double*>(smem + (size_t)warp * cec_eval_warp_bytes(dim, A.bufs));
+    double* W = X + (size_t)kCecRows * cs;
+    double* xrow = X + (size_t)q * cs;
+    const double* ew = A.O.table_len >= dim ? A.O.table : nullptr;  // ELLIPS weights (host libm)
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    const int ntiles = (A.n_rows + kCecRows - 1) / kCecRows;
+    for (int tile = blockIdx.x * nwarps + warp; tile < ntiles; tile += gridDim.x * nwarps) {
+        const int r0 = tile * kCecRows;
+        const int nb = min(kCecRows, A.n_rows - r0);
+        const int r = r0 + q;
+        const bool live = q < nb;
+        uint8_t cur = 0;
+        const double* src = nullptr;
+        if (live) {
+            if constexpr (SEL) {
+                cur = A.sel[r];
+                src = (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld;  // the slot's alternate buffer
+            } else {
+                src = A.out_pos + (size_t)r * A.ld;
+            }
+        }
+        for (int i = t; i < n4; i += 4) xrow[i] = (live && i < dim) ? src[i] : 0.0;
+        const bool ok = live && A.cand_ok[r] != 0;
+        __syncwarp();
+        const double nf = cec_eval_quad<NT>(A.O.cec, X, W, cs, dim, lane, ew);
+        bool acc = false;
+        if (live && t == 0) {
+            const double fit_i = A.fit[r];
+            double kept = fit_i;
+            bool warned = false;
+            if (ok && isfinite(nf)) {
+                acc = nf < fit_i;
+                if (acc) kept = nf;
+            } else {
+                warned = true;
+            }
+            A.out_fit[r] = kept;
+            if constexpr (SEL) {
+                A.sel_next[r] = acc ? (uint8_t)(cur ^ 1) : cur;
+            } else {
+                if (A.out_acc) A.out_acc[r] = acc ? 1 : 0;
+                if (A.out_warn) A.out_warn[r] = warned ? 1 : 0;
+            }
+            const unsigned long long k = sort_key(kept);
+            my_min = k < my_min ? k : my_min;
+            my_warn += warned ? 1u : 0u;
+        }
+        if constexpr (!SEL) {
+            unsigned rej = __ballot_sync(kFull, live && t == 0 && !acc);
+            while (rej) {
+                const int qq = (__ffs(rej) - 1) >> 2;
+                rej &= rej - 1;
+                const double* x = A.pos + (size_t)(r0 + qq) * A.ld;
+                double* dst = A.out_pos + (size_t)(r0 + qq) * A.ld;
+                for (int d = lane; d < dim; d += 32) dst[d] = x[d];
+            }
+        }
+        __syncwarp();
+    }
+    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
+}
+
 // Kernel getters (defined in the instantiating TUs).
 const void* pick_update_sel(int dim);
 const void* pick_update_dense(int dim);
 const void* pick_run_batch(int dim);
+const void* pick_cec_eval(bool sel, int dim);
 
 }  // namespace apo

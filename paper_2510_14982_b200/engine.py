@@ -246,6 +246,13 @@ class DeviceRun:
         _lib.check(self.lib.apo_run_profile_read(self.handle, C.byref(ms), C.byref(n)), "apo_run_profile_read")
         return ms.value, n.value
 
+    def profile_split(self):
+        """(candidate-kernel ms, CEC evaluation-kernel ms, iterations) since profile()."""
+        a, b, n = C.c_double(), C.c_double(), C.c_int64()
+        _lib.check(self.lib.apo_run_profile_split(self.handle, C.byref(a), C.byref(b), C.byref(n)),
+                   "apo_run_profile_split")
+        return a.value, b.value, n.value
+
     def close(self):
         if self.handle:
             self.lib.apo_run_destroy(self.handle)

@@ -169,7 +169,15 @@ class DeviceObjective:
         if obj.data is not None and hasattr(obj.data, "arrays"):  # CEC2022
             shift, rot, shuffle = obj.data.arrays(dim)
             rot_t = np.ascontiguousarray(np.transpose(rot, (0, 2, 1)))
-            for field, arr in (("shift", shift), ("rot_t", rot_t), ("shuffle", shuffle)):
+            arrays = [("shift", shift), ("rot_t", rot_t), ("shuffle", shuffle)]
+            if dim <= 104:  # zero-padded M^T for the DMMA evaluation kernel (include/apo_b200.h)
+                nt = 2 if dim <= 16 else 4 if dim <= 32 else 7 if dim <= 56 else 13
+                n4 = (dim + 3) // 4 * 4
+                pad = np.zeros((rot_t.shape[0], n4, 8 * nt))
+                pad[:, :dim, :dim] = rot_t
+                arrays.append(("rot_pad", pad))
+                table = elliptic_weights(dim)  # ELLIPS weights 10^(6i/(D-1)), host libm like the oracle
+            for field, arr in arrays:
                 t = torch.as_tensor(np.array(arr), device=dev)
                 self.keep.append(t)
                 setattr(self.struct, field, t.data_ptr())

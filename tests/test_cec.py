@@ -79,7 +79,7 @@ def test_teacher_forced_step_matches_oracle(fn):
     from paper_2510_14982_b200.kernels import get_backend
 
     name = f"cec2022_f{fn}"
-    for ps, dim in ((100, 20), (3000, 50)):
+    for ps, dim in ((100, 20), (3000, 50), (2000, 100), (300, 12)):
         cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=50, seed=fn)
         pos, fit = oracle.initialize(fn, ps, dim, -100.0, 100.0, name)
         order = oracle.argsort_stable(fit)
