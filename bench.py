@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c4", choices=["c4", "c2"])
-    ap.add_argument("--objective", default="rosenbrock")
+    ap.add_argument("--objective", default="cec2022_f6")
     ap.add_argument("--ps", type=int, default=1_000_000)
     ap.add_argument("--dim", type=int, default=100)
     ap.add_argument("--no-e2e", action="store_true")
@@ -181,7 +181,26 @@ def bytes_per_eval(dim: int, p_auto: float, npairs: int = 1) -> float:
 # ---------------------------------------------------------------------------
 
 
-def bench_ours(args, rank, world, local):
+def fp64_peak():
+    """Measured FP64 DMMA peak (tools/fp64_peak.cu on this pool's B200, profiles/r01_fp64_peak.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as fh:
+            d = json.load(fh)
+        return float(d["dmma_tflops_4chain"]), "measured (tools/fp64_peak.cu)"
+    except Exception:
+        return 37.0, "fallback"
+
+
+def rotated_components(name: str) -> int:
+    """Rotations per evaluation (the D x D contractions k_cec_eval runs)."""
+    if not name.startswith("cec2022_f"):
+        return 0
+    fn = int(name[len("cec2022_f"):])
+    return {9: 3, 10: 1, 11: 5, 12: 6}.get(fn, 1)
+
+
+def c4_measure(args, name, rank, world, local, K, W):
+    """Device-resident C4 run: CUDA-event time of K iterations + per-kernel split."""
     import torch
 
     import paper_2510_14982_b200 as pz
@@ -189,10 +208,9 @@ def bench_ours(args, rank, world, local):
     from paper_2510_14982_b200.core import iteration_scalars
     from paper_2510_14982_b200.engine import DeviceRun
 
-    torch.cuda.set_device(local)
-    ps, dim, K, W = args.ps, args.dim, args.steps, args.warmup
+    ps, dim = args.ps, args.dim
     T = max(100, K + W)
-    obj = pz.get_objective(args.objective)
+    obj = pz.get_objective(name)
     cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=T, seed=rank)
     run = DeviceRun(cfg, obj)
     run.initialize()
@@ -212,56 +230,91 @@ def bench_ours(args, rank, world, local):
     barrier(world)
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
-    upd_ms, launches = run.profile_read()
+    cand_ms, eval_ms, launches = run.profile_split()
     max_ms = max_over_ranks(ms, world)
-    value = world * ps * K / (max_ms / 1e3)
-    # algorithmic bytes of the timed launches (rank 0's population; ranks are statistically identical)
+    # algorithmic bytes of the timed candidate launches (population independent op mix)
     dev = torch.device("cuda", local)
     in_dr = torch.empty(ps, dtype=torch.uint8, device=dev)
-    total_bytes = 0.0
-    p_autos = []
+    total_bytes, p_autos = 0.0, []
     for t in range(W, W + K):
         _lib.check(_lib.load().apo_select_dr(cfg.seed, t + 1, ps, cfg.pf_max, _lib.ptr(in_dr), None,
                                              _lib.stream_handle()))
         p_auto = op_mix(cfg.seed, t + 1, ps, iteration_scalars(t, T)[0], in_dr.cpu().numpy().astype(bool))
         p_autos.append(p_auto)
         total_bytes += ps * bytes_per_eval(dim, p_auto, cfg.neighbor_pairs)
-    per_launch = total_bytes / K
-    kern_s = upd_ms / 1e3 / max(launches, 1)
-    peaks, peak_kind = measured_peaks()
-    achieved = per_launch / kern_s / 1e9
-    traffic = profile_traffic("c4", args.objective)
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
-                "peak_source": peak_kind, "kernel": "k_update<true>",
-                "kernel_ms_avg": round(upd_ms / max(launches, 1), 4),
-                "kernel_share_of_step": round(upd_ms / ms, 4),
-                "bytes_per_launch": per_launch, "bytes_per_eval": round(per_launch / ps, 1),
-                "p_auto_mean": round(float(np.mean(p_autos)), 4)}
-    result = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (keyed-hash initial population, seed = rank)",
-        "config": {"workload": f"C4: single population ps={ps} D={dim} objective={args.objective}"
-                               + (" (stand-in for CEC2022 F6/F10)" if args.objective in pz.FUNCTION_NAMES else ""),
-                   "ps": ps, "dim": dim, "iterations_per_step": 1, "max_iterations": T,
-                   "l2": "inputs larger than L2 (800 MB population)",
-                   "parallelism": f"independent runs x{world}" if world > 1 else "single GPU",
-                   "rng": "keyed fmix64 (bit-exact with the reference)"},
-        "roofline": roofline,
-        "clocks": clk,
-        # my kernels per iteration: k_make_keys, k_dr_draw, k_dr_resolve, k_update (+ CUB radix-sort passes)
-        "gpu_launches": 4 * K,
-    }
     run.close()
     del run
     torch.cuda.empty_cache()
+    n = max(launches, 1)
+    peaks, peak_kind = measured_peaks()
+    cand_s = cand_ms / 1e3 / n
+    per_launch = total_bytes / K
+    cand_gbs = per_launch / cand_s / 1e9
+    kernels = [{"kernel": "k_update_group<SEL>" + (" (candidates only)" if eval_ms > 0 else " (fused)"),
+                "bound": "hbm", "achieved": round(cand_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(cand_gbs / peaks["hbm_gbs"], 4), "peak_source": peak_kind,
+                "kernel_ms_avg": round(cand_ms / n, 4), "kernel_share_of_step": round(cand_ms / ms, 4),
+                "bytes_per_launch": per_launch, "bytes_per_eval": round(per_launch / ps, 1),
+                "p_auto_mean": round(float(np.mean(p_autos)), 4),
+                "traffic": profile_traffic("c4", name)}]
+    if eval_ms > 0:
+        nrot = rotated_components(name)
+        flops = ps * nrot * 2.0 * dim * dim
+        eval_s = eval_ms / 1e3 / n
+        tf = flops / eval_s / 1e12
+        pk, pk_src = fp64_peak()
+        kernels.append({"kernel": "k_cec_eval (DMMA f64 m8n8k4 rotation + basic + greedy select)",
+                        "bound": "tensor", "achieved": round(tf, 2), "peak": pk, "unit": "TFLOP/s",
+                        "frac": round(tf / pk, 4), "peak_source": pk_src, "kernel_ms_avg": round(eval_ms / n, 4),
+                        "kernel_share_of_step": round(eval_ms / ms, 4), "flops_per_launch": flops,
+                        "flops_per_eval": nrot * 2.0 * dim * dim,
+                        "also_reads_bytes_per_eval": 8 * dim + 16, "traffic": profile_traffic("c4eval", name)})
+    dominant = max(kernels, key=lambda k: k["kernel_ms_avg"])
+    return dict(cfg=cfg, obj=obj, ms=ms, max_ms=max_ms, clocks=clk, kernels=kernels, dominant=dominant,
+                launches=launches)
+
+
+def c4_workload(name, ps, dim):
+    return f"C4: single population ps={ps} D={dim} objective={name} (synthetic CEC2022 data)"
+
+
+def bench_ours(args, rank, world, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    K, W = args.steps, args.warmup
+    m = c4_measure(args, args.objective, rank, world, local, K, W)
+    ps, dim = args.ps, args.dim
+    value = world * ps * K / (m["max_ms"] / 1e3)
+    roofline = dict(m["dominant"])
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": m["max_ms"] / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (keyed-hash initial population, seed = rank; synthetic CEC2022 "
+                                "shift/rotation/shuffle data, cec2022.py)",
+        "config": {"workload": c4_workload(args.objective, ps, dim), "ps": ps, "dim": dim,
+                   "iterations_per_step": 1, "max_iterations": max(100, K + W),
+                   "l2": "inputs larger than L2 (2 x 800 MB population buffers)",
+                   "parallelism": f"independent populations x{world} (seed = rank)" if world > 1 else "single GPU",
+                   "rng": "keyed fmix64 (bit-exact with the reference)"},
+        "roofline": roofline,
+        "roofline_kernels": m["kernels"],
+        "clocks": m["clocks"],
+        # per iteration: k_make_keys, k_dr_draw, k_dr_resolve, k_update_group (+ k_cec_eval), CUB sort passes
+        "gpu_launches": (4 + (1 if len(m["kernels"]) > 1 else 0)) * K,
+    }
+    if not args.no_suite:
+        other = "cec2022_f10" if args.objective != "cec2022_f10" else "cec2022_f6"
+        m2 = c4_measure(args, other, rank, world, local, K, W)
+        result["c4_" + other.split("_")[1]] = {
+            "value": world * ps * K / (m2["max_ms"] / 1e3), "unit": UNIT, "ms_per_step": m2["max_ms"] / K,
+            "workload": c4_workload(other, ps, dim), "roofline_kernels": m2["kernels"]}
     if not args.no_e2e:
-        result["e2e"] = bench_e2e(cfg, obj, K, rank, world)
+        result["e2e"] = bench_e2e(m["cfg"], m["obj"], K, rank, world)
     if not args.no_suite and rank == 0:
         result["suite_c2"] = bench_suite(world)
     if rank == 0 and world == 1 and not args.no_cpu:
-        result["cpu_baseline"] = cpu_baseline(cfg, args.objective)
+        result["cpu_baseline"] = cpu_baseline(m["cfg"], args.objective)
     return result
 
 
@@ -287,26 +340,28 @@ def bench_e2e(cfg, obj, K, rank, world):
 
 
 def bench_suite(world):
-    """BASELINE config 2 shape: 360 independent runs (D=20, ps=100, 1000 iterations), one CTA per run."""
+    """BASELINE config 2: CEC2022 F1-F12 x 30 seeds (360 independent runs), D=20, ps=100, T=1000,
+    one CTA per run with the population resident in shared memory (rank 0's GPU)."""
     import torch
 
     import paper_2510_14982_b200 as pz
 
     cfg = pz.ApoConfig(ps=100, dim=20, bounds=pz.Bounds(-100.0, 100.0, 20), max_iterations=1000)
-    names = [n for n in ("sphere", "bent_cigar", "high_conditioned_elliptic", "hgbat", "rosenbrock", "griewank")
-             for _ in range(60)]
-    seeds = list(range(len(names)))
-    pz.run_batch(cfg, names[:16], seeds[:16], want_trace=False, device_out=True)
+    names = [f"cec2022_f{k}" for k in range(1, 13) for _ in range(30)]
+    seeds = [s for _ in range(12) for s in range(30)]
+    pz.run_batch(cfg, names[:24], seeds[:24], want_trace=False, device_out=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    pz.run_batch(cfg, names, seeds, want_trace=False, device_out=True)
+    res = pz.run_batch(cfg, names, seeds, want_trace=False, device_out=True)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     evals = len(names) * cfg.ps * cfg.max_iterations
+    best = res.best_fitness.cpu().numpy().reshape(12, 30)
     return {"value": evals / (ms / 1e3), "unit": UNIT, "ms": ms, "runs": len(names),
-            "workload": "C2 shape: 6 reference functions x 60 seeds, D=20, ps=100, T=1000 (CEC2022 F1-F12 pending)",
+            "workload": "C2: CEC2022 F1-F12 (synthetic data) x 30 seeds, D=20, ps=100, T=1000, one CTA per run",
+            "median_best_minus_fstar": [float(np.median(best[k]) - pz.cec2022.FSTAR[k]) for k in range(12)],
             "gpus": 1}
 
 

@@ -6,7 +6,7 @@
  * module exposes NAME, max_workers() and run_updates(...).  The reference's
  * only compiled code is the numba dispatcher that run_updates calls
  * (kernels/numba_backend.py:367-371, `_step_parallel(*args)` with the flat
- * argument tuple built at :425-433); apo_run_updates() below takes exactly
+ * argument tuple built at :358-366); apo_run_updates() below takes exactly
  * that tuple, as device pointers, plus sizes and a stream.  The Python
  * backend paper_2510_14982_b200/kernels/cuda_backend.py binds it with
  * ctypes (see INTEGRATION.md for the binding a reference maintainer adds).
@@ -19,7 +19,7 @@
  *    available from apo_last_error() (thread-local); invalid arguments are
  *    rejected with APO_EINVAL before any launch;
  *  - no function reads or writes its input population (numba_backend.py
- *    :401-404 "Inputs are read only"); callers own all outputs.
+ *    :334-337 "Inputs are read only"); callers own all outputs.
  */
 #ifndef APO_B200_H
 #define APO_B200_H
@@ -71,7 +71,7 @@ int apo_device_count(void);
  * One iteration's per-individual phase over a rank-sorted snapshot.
  * Replaces numba_backend.run_updates (kernels/numba_backend.py:323-372):
  * same inputs (positions [ps, dim] row-major, rank r+1 in row r; fitness
- * [ps]; in_dr [ps] bool by rank), same flat scalars (:425-433), same
+ * [ps]; in_dr [ps] bool by rank), same flat scalars (:358-366), same
  * outputs (new positions/fitness in rank order, accepted, warned).
  * p_dr [ps] holds 0.5*(1-cos((1-i/ps)*pi)) per rank (numba_backend.py:
  * 173-175), computed by the host with libm so the decision threshold is
