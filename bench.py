@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c4", "c2"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2", "c3"])
     ap.add_argument("--objective", default="cec2022_f6")
     ap.add_argument("--ps", type=int, default=1_000_000)
     ap.add_argument("--dim", type=int, default=100)
@@ -313,6 +313,7 @@ def bench_ours(args, rank, world, local):
         result["e2e"] = bench_e2e(m["cfg"], m["obj"], K, rank, world)
     if not args.no_suite and rank == 0:
         result["suite_c2"] = bench_suite(world)
+        result["suite_c3"] = bench_c3()
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(m["cfg"], args.objective)
     return result
@@ -363,6 +364,61 @@ def bench_suite(world):
             "workload": "C2: CEC2022 F1-F12 (synthetic data) x 30 seeds, D=20, ps=100, T=1000, one CTA per run",
             "median_best_minus_fstar": [float(np.median(best[k]) - pz.cec2022.FSTAR[k]) for k in range(12)],
             "gpus": 1}
+
+
+def bench_c3():
+    """BASELINE config 3: multilevel Otsu and Kapur (k = 2..5 thresholds) on a synthetic 4096x4096 8-bit
+    image; ps=100, T=1000, 30 seeds per (method, k), the 8 batches on 8 concurrent streams."""
+    import torch
+
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200 import imaging
+
+    rnd = np.random.default_rng(0)
+    n = 4096 * 4096
+    comp = rnd.random(n) < 0.5
+    px = np.where(comp, rnd.normal(70.0, 12.0, n), rnd.normal(190.0, 14.0, n))
+    img = np.clip(np.rint(px), 0, 255).astype(np.uint8)
+    dimg = torch.as_tensor(img).cuda()
+    imaging.histogram_device(dimg)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 20
+    for _ in range(reps):
+        counts = imaging.histogram_device(dimg)
+    e1.record()
+    torch.cuda.synchronize()
+    hist_ms = e0.elapsed_time(e1) / reps
+    jobs = []
+    for method in ("otsu", "kapur"):
+        for k in (2, 3, 4, 5):
+            obj = imaging.multilevel_objective(counts, k, method)
+            cfg = pz.ApoConfig(ps=100, dim=k, bounds=pz.Bounds(0.0, 255.0, k), max_iterations=1000)
+            jobs.append((method, k, obj, cfg))
+    streams = [torch.cuda.Stream() for _ in jobs]
+    for (m, k, obj, cfg), st in zip(jobs, streams):  # warm-up (compiles nothing; first-launch costs)
+        pz.run_batch(cfg, [obj] * 2, [0, 1], want_trace=False, device_out=True, stream=st)
+    torch.cuda.synchronize()
+    e0.record()
+    cur = torch.cuda.current_stream()
+    outs = []
+    for (m, k, obj, cfg), st in zip(jobs, streams):
+        st.wait_stream(cur)
+        outs.append(pz.run_batch(cfg, [obj] * 30, list(range(30)), want_trace=False, device_out=True, stream=st))
+    for st in streams:
+        cur.wait_stream(st)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    evals = len(jobs) * 30 * 100 * 1000
+    best = {f"{m}_k{k}": {"thresholds": list(imaging.thresholds_of(o.best_position[0].cpu().numpy())),
+                          "value": -float(o.best_fitness.min())}
+            for (m, k, _, _), o in zip(jobs, outs)}
+    return {"value": evals / (ms / 1e3), "unit": UNIT, "ms": ms, "runs": len(jobs) * 30,
+            "workload": "C3: Otsu + Kapur, k=2..5, synthetic 4096x4096 bimodal u8 image, ps=100, T=1000, 30 seeds",
+            "histogram": {"ms": hist_ms, "gbs": n / (hist_ms / 1e3) / 1e9, "kernel": "k_histogram_u8"},
+            "best": best, "prefix_tables": "shared memory (k_run_batch stages the 515-entry table per CTA)"}
 
 
 def cpu_baseline(cfg, objective, max_seconds=25.0):
@@ -445,11 +501,11 @@ def main():
             print(json.dumps(res), flush=True)
         return
     rank, world, local = dist_setup("nccl")
-    if args.workload == "c2":
+    if args.workload in ("c2", "c3"):
         import torch
 
         torch.cuda.set_device(local)
-        res = bench_suite(world)
+        res = bench_suite(world) if args.workload == "c2" else bench_c3()
         if rank == 0:
             print(json.dumps({"metric": METRIC, **res, "n_gpus": world, "steps": 1, "warmup": 1}), flush=True)
         return

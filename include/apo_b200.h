@@ -43,6 +43,13 @@ extern "C" {
 #define APO_OBJ_ROSENBROCK 4
 #define APO_OBJ_GRIEWANK 5
 #define APO_OBJ_TABLE 6 /* table[round_half_up(x0)] (objectives.py:183-192, 213-219) */
+/* Multilevel thresholds (no reference counterpart): dim = k <= 32
+ * thresholds in [0, 255]; table = the 515-entry prefix table written by
+ * apo_threshold_tables (classes [0,t_0], [t_0+1,t_1], ..., [t_{k-1}+1, 255],
+ * the k = 1 case being the reference's class convention, imaging.py:203-223). */
+#define APO_OBJ_OTSU_ML 7  /* -(between-class variance) */
+#define APO_OBJ_KAPUR_ML 8 /* -(sum of class entropies) */
+#define APO_THRESHOLD_TABLE_LEN 515
 /* CEC2022 F1..F12: code = APO_OBJ_CEC2022_BASE + F (no reference counterpart,
  * SPEC.md:146; definitions in csrc/apo_cec.cuh, data from cec2022.py). */
 #define APO_OBJ_CEC2022_BASE 100
@@ -110,6 +117,12 @@ int apo_sort_order(const double *fitness, int64_t n, int32_t *order, void *strea
  * set size through count_host (nullable). */
 int apo_select_dr(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_max, uint8_t *in_dr,
                   int64_t *count_host, void *stream);
+
+/* Prefix tables of a 256-bin histogram for APO_OBJ_OTSU_ML (method 0) or
+ * APO_OBJ_KAPUR_ML (method 1): table[0] = N, table[1+i] = sum_{v<i} count_v,
+ * table[258+i] = sum_{v<i} v count_v (Otsu) / sum_{v<i} p_v ln p_v (Kapur),
+ * i = 0..256 (generalises imaging.variance_table, imaging.py:226-228). */
+int apo_threshold_tables(const int64_t *counts, int method, double *table, void *stream);
 
 /* 256-bin histogram of an 8-bit image (imaging.histogram, imaging.py:197-200). */
 int apo_histogram_u8(const uint8_t *pixels, int64_t n, int64_t *counts, void *stream);

@@ -10,7 +10,7 @@ this package; the product package never does.
 Parity pin: tests/test_oracle_golden.py checks every entry point below
 against vectors the reference itself produced (tests/golden/).  The
 CEC2022 and multilevel-threshold restatements (cec_oracle.c,
-imaging_oracle.c) have no reference counterpart: **parity unpinned** for
+threshold_oracle.c) have no reference counterpart: **parity unpinned** for
 those.
 """
 
@@ -28,7 +28,7 @@ LIB_PATH = os.path.join(HERE, "liboracle_apo.so")
 
 COORDINATOR_INDEX = (1 << 64) - 1
 CODES = {"sphere": 0, "bent_cigar": 1, "high_conditioned_elliptic": 2, "hgbat": 3, "rosenbrock": 4,
-         "griewank": 5, "table": 6}
+         "griewank": 5, "table": 6, "otsu_ml": 7, "kapur_ml": 8}
 
 _lib = None
 
@@ -97,7 +97,22 @@ _EXTRA_DECLS: dict = {
     "or_cec_eval_batch": (None, [C.c_int, _P, _I, C.c_int, _P, _P, _P, _P, C.c_int]),
     "or_cec_spec": (None, [C.c_int, _P]),
     "or_cec_ncomp": (C.c_int, [C.c_int]),
+    "or_threshold_tables": (None, [_P, C.c_int, _P]),
+    "or_threshold_eval": (C.c_double, [C.c_int, _P, _I, _P]),
 }
+
+
+def threshold_tables(counts, method: str) -> np.ndarray:
+    """Prefix tables of a 256-bin histogram (threshold_oracle.c layout): method 'otsu' or 'kapur'."""
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    tab = np.zeros(515)
+    lib().or_threshold_tables(_ptr(c), 0 if method == "otsu" else 1, _ptr(tab))
+    return tab
+
+
+def threshold_eval(method: str, x, tab) -> float:
+    x = _f64(np.atleast_1d(x))
+    return float(lib().or_threshold_eval(0 if method == "otsu" else 1, _ptr(x), x.size, _ptr(_f64(tab))))
 
 
 def cec_eval(fn: int, x, nthreads: int = 1) -> np.ndarray:
@@ -176,6 +191,8 @@ def objective_table(name: str, dim: int, table=None):
         fn = int(name[len("cec2022_f"):])
         return 100 + fn, cec_packed(fn, dim)
     code = CODES[name]
+    if code in (7, 8):
+        return code, _f64(table)
     if code == 2:
         return code, elliptic_weights(dim)
     if code == 6:

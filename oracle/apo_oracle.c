@@ -97,9 +97,12 @@ void or_randperm(int64_t n, int64_t k, uint64_t base, uint64_t ctr0, int64_t *ou
 /* ---------------------------------------------------------------------------
  * Objectives: numba_backend.py:93-138 (== objectives.py:105-152, 213-219)
  * ------------------------------------------------------------------------- */
+double or_threshold_eval(int method, const double *x, int64_t k, const double *tab);
+
 double or_eval(int64_t code, const double *x, int64_t n, const double *table, int64_t tlen) {
     double s, s1, s2, p;
     if (code > 100) return cec_packed((int)(code - 100), x, n, table);
+    if (code == 7 || code == 8) return or_threshold_eval((int)(code - 7), x, n, table); /* multilevel Otsu / Kapur */
     switch (code) {
     case SPHERE:
         s = 0.0;

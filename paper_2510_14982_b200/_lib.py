@@ -111,6 +111,7 @@ PROTOTYPES = {
     "apo_sort_order": (_INT, [_P, _I, _P, _P]),
     "apo_select_dr": (_INT, [_U, _U, _I, _D, _P, C.POINTER(C.c_int64), _P]),
     "apo_histogram_u8": (_INT, [_P, _I, _P, _P]),
+    "apo_threshold_tables": (_INT, [_P, _INT, _P, _P]),
     "apo_run_create": (_INT, [C.POINTER(C.c_void_p), _I, _I, _I, _U, _I, _D, _D, _D, _D, C.POINTER(apo_objective),
                               _P, _P, _P]),
     "apo_run_initialize": (_INT, [_P]),

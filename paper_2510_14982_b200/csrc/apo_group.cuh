@@ -426,7 +426,7 @@ __device__ __forceinline__ void write_terms(const ObjDesc& O, double* T1, double
         T2[d] = cos(c / sqrt((double)d + 1.0));
         break;
     default:
-        if (O.code >= OBJ_CEC_BASE) {
+        if (O.code >= OBJ_CEC_BASE || O.code == OBJ_OTSU_ML || O.code == OBJ_KAPUR_ML) {
             T1[d] = c;
         } else if (d == 0) {
             long long idx = (long long)floor(c + 0.5);
@@ -473,6 +473,9 @@ __device__ inline double fold_terms(const ObjDesc& O, const double* T1, const do
         }
         return 1.0 + s / 4000.0 - p;
     }
+    case OBJ_OTSU_ML:
+    case OBJ_KAPUR_ML:
+        return threshold_ml(O.code, T1, dim, O.table);
     default:
         return T1[0];
     }

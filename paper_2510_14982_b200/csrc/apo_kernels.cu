@@ -93,7 +93,11 @@ ObjDesc to_desc(const apo_objective* o) {
 int check_objective(const apo_objective* o, int64_t dim) {
     APO_CHECK(o != nullptr, "objective descriptor is NULL");
     const bool cec = o->code > APO_OBJ_CEC2022_BASE && o->code <= APO_OBJ_CEC2022_BASE + 12;
-    APO_CHECK(cec || (o->code >= APO_OBJ_SPHERE && o->code <= APO_OBJ_TABLE), "unsupported objective code");
+    APO_CHECK(cec || (o->code >= APO_OBJ_SPHERE && o->code <= APO_OBJ_KAPUR_ML), "unsupported objective code");
+    if (o->code == APO_OBJ_OTSU_ML || o->code == APO_OBJ_KAPUR_ML) {
+        APO_CHECK(o->table && o->table_len >= APO_THRESHOLD_TABLE_LEN, "threshold objective needs the 515-entry table");
+        APO_CHECK(dim >= 1 && dim <= kThresholdMaxK, "multilevel thresholding supports 1..32 thresholds");
+    }
     if (cec) {
         APO_CHECK(o->shift && o->rot_t, "CEC2022 objectives need shift and rotation data");
         const int fn = o->code - APO_OBJ_CEC2022_BASE;
@@ -249,6 +253,30 @@ __global__ void k_histogram_u8(const uint8_t* __restrict__ px, long long n, unsi
         unsigned long long s = 0;
         for (int w = 0; w < kWarps; w++) s += h[w][b];
         if (s) atomicAdd(&counts[b], s);
+    }
+}
+
+// Prefix tables for the multilevel threshold objectives, one thread in
+// histogram order (the order oracle/threshold_oracle.c sums in).
+__global__ void k_threshold_tables(const long long* __restrict__ counts, int method, double* __restrict__ tab) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    long long n = 0;
+    for (int v = 0; v < 256; v++) n += counts[v];
+    tab[0] = (double)n;
+    long long c = 0;
+    double s = 0.0;
+    tab[1] = 0.0;
+    tab[258] = 0.0;
+    for (int v = 0; v < 256; v++) {
+        c += counts[v];
+        tab[2 + v] = (double)c;
+        if (method == 0) {
+            s += (double)v * (double)counts[v];
+        } else if (counts[v] > 0) {
+            const double p = (double)counts[v] / (double)n;
+            s += p * log(p);
+        }
+        tab[259 + v] = s;
     }
 }
 
@@ -572,6 +600,13 @@ int apo_histogram_u8(const uint8_t* pixels, int64_t n, int64_t* counts, void* st
     const long long cap = 4LL * num_sms();
     if (g < 1) g = 1;
     k_histogram_u8<<<(int)(g < cap ? g : cap), kThreads, 0, st>>>(pixels, n, (unsigned long long*)counts);
+    APO_CUDA(cudaGetLastError());
+    return APO_OK;
+}
+
+int apo_threshold_tables(const int64_t* counts, int method, double* table, void* stream) {
+    APO_CHECK(counts && table && (method == 0 || method == 1), "bad arguments");
+    k_threshold_tables<<<1, 32, 0, as_stream(stream)>>>((const long long*)counts, method, table);
     APO_CUDA(cudaGetLastError());
     return APO_OK;
 }
@@ -914,11 +949,14 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     A.final_fit = final_fit;
     A.warnings = (long long*)warnings;
     A.cec_bufs = 0;
+    A.tab_smem = 0;
     for (int64_t k = 0; k < nruns; k++) {
         const int cb = cec_bufs_for(objectives_host[k].code);
         if (cb > A.cec_bufs) A.cec_bufs = cb;
+        if (objectives_host[k].code == APO_OBJ_OTSU_ML || objectives_host[k].code == APO_OBJ_KAPUR_ML)
+            A.tab_smem = APO_THRESHOLD_TABLE_LEN;
     }
-    const BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs);
+    const BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs, A.tab_smem);
     {
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);

@@ -164,11 +164,12 @@ struct BatchArgs {
     double* final_pos;
     double* final_fit;
     long long* warnings;
-    int cec_bufs;  // max over the batch's objectives of cec_bufs_for(code)
+    int cec_bufs;   // max over the batch's objectives of cec_bufs_for(code)
+    int tab_smem;   // doubles of threshold prefix table staged in shared memory (0 = none)
 };
 
 struct BatchLayout {
-    size_t pos0, pos1, fit0, fit1, keys, order, rankof, newrank, chead, cprev, crj, cbits, warps, total;
+    size_t pos0, pos1, fit0, fit1, keys, order, rankof, newrank, chead, cprev, crj, cbits, tab, warps, total;
 };
 
 __host__ __device__ inline size_t batch_warp_bytes(int dim, int cec_bufs) {
@@ -178,7 +179,8 @@ __host__ __device__ inline size_t batch_warp_bytes(int dim, int cec_bufs) {
     return gs > ws ? gs : ws;
 }
 
-__host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int nwarps, int cec_bufs) {
+__host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int nwarps, int cec_bufs,
+                                                int tab_smem = 0) {
     BatchLayout L;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -198,6 +200,7 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
     L.cprev = take(4 * (size_t)ps);
     L.crj = take(4 * (size_t)ps);
     L.cbits = take(4 * (size_t)((ps + 31) / 32));
+    L.tab = take(8 * (size_t)tab_smem);
     L.warps = take(batch_warp_bytes(dim, cec_bufs) * (size_t)nwarps);
     L.total = o;
     return L;
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int run = blockIdx.x;
     const int ps = A.ps, dim = A.dim, ld = A.ld;
-    const BatchLayout L = batch_layout(ps, dim, ld, nwarps, A.cec_bufs);
+    const BatchLayout L = batch_layout(ps, dim, ld, nwarps, A.cec_bufs, A.tab_smem);
     double* pos[2] = {reinterpret_cast<double*>(smem + L.pos0), reinterpret_cast<double*>(smem + L.pos1)};
     double* fit[2] = {reinterpret_cast<double*>(smem + L.fit0), reinterpret_cast<double*>(smem + L.fit1)};
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem + L.keys);
@@ -229,7 +232,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
     const GroupScratch g = group_scratch(wbase, dim, false, A.cec_bufs);
     const WarpScratch ws = MAXC >= 0 ? g.ws : warp_scratch(wbase, dim);
     const uint64_t seed = A.seeds[run];
-    const ObjDesc O = A.objs[run];
+    ObjDesc O = A.objs[run];
+    if (A.tab_smem > 0 && (O.code == OBJ_OTSU_ML || O.code == OBJ_KAPUR_ML)) {
+        // the 256-bin prefix tables live in shared memory for the whole run
+        double* tab = reinterpret_cast<double*>(smem + L.tab);
+        for (int k = threadIdx.x; k < O.table_len && k < A.tab_smem; k += blockDim.x) tab[k] = O.table[k];
+        O.table = tab;
+        __syncthreads();
+    }
     double* trace = A.trace ? A.trace + (size_t)run * (A.n_iters + 1) : nullptr;
 
     // initialisation (engine.py:116-139); the init scratch aliases this warp's group scratch

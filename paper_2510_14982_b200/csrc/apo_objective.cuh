@@ -19,7 +19,12 @@ enum ObjCode : int {
     OBJ_ROSENBROCK = 4,
     OBJ_GRIEWANK = 5,
     OBJ_TABLE = 6,
+    OBJ_OTSU_ML = 7,   // multilevel Otsu over the prefix tables (apo_threshold_tables)
+    OBJ_KAPUR_ML = 8,  // multilevel Kapur
 };
+
+constexpr int kThresholdTabLen = 515;
+constexpr int kThresholdMaxK = 32;
 
 // Objective descriptor; all pointers are device pointers.
 struct ObjDesc {
@@ -45,6 +50,49 @@ __device__ __forceinline__ double seq_sum(const double* t, int from, int to) {
     }
     if (d < to) s += t[d];
     return s;
+}
+
+// Multilevel thresholding objective of k = dim thresholds x (one lane).
+// Thresholds t_j = clamp(round_half_up(x_j), 0, 255) sorted ascending;
+// classes [0,t_0], [t_0+1,t_1], ..., [t_{k-1}+1, 255]; empty classes add 0.
+// tab: [N | C[0..256] | S[0..256]] with C = prefix counts and S = prefix
+// v*count (Otsu) or prefix p ln p (Kapur).  Same expression order as
+// oracle/threshold_oracle.c.  f = -(between-class variance) or -(entropy).
+__host__ __device__ inline double threshold_ml(int code, const double* x, int k, const double* tab) {
+    int t[kThresholdMaxK];
+    for (int j = 0; j < k; j++) {
+        const double r = floor(x[j] + 0.5);
+        int v = !(r >= 0.0) ? 0 : r > 255.0 ? 255 : (int)r;
+        int i = j;
+        while (i > 0 && t[i - 1] > v) {
+            t[i] = t[i - 1];
+            i--;
+        }
+        t[i] = v;
+    }
+    const double N = tab[0];
+    const double* C = tab + 1;
+    const double* S = tab + 258;
+    const double mu_t = S[256] / N;
+    double f = 0.0;
+    int lo = 0;
+    for (int c = 0; c <= k; c++) {
+        const int hi = c < k ? t[c] : 255;
+        if (hi >= lo) {
+            const double nc = C[hi + 1] - C[lo];
+            if (nc > 0.0) {
+                const double w = nc / N;
+                if (code == OBJ_OTSU_ML) {
+                    const double d = (S[hi + 1] - S[lo]) / nc - mu_t;
+                    f += w * (d * d);
+                } else {
+                    f += log(w) - (S[hi + 1] - S[lo]) / w;
+                }
+            }
+        }
+        lo = hi + 1;
+    }
+    return -f;
 }
 
 // c: candidate [dim] (shared), t / aux: scratch [dim] (shared).  Returns the
@@ -100,6 +148,10 @@ __device__ inline double eval_warp(const ObjDesc& O, const double* c, double* t,
             }
             f = 1.0 + s / 4000.0 - p;
         }
+        break;
+    case OBJ_OTSU_ML:
+    case OBJ_KAPUR_ML:
+        if (lane == 0) f = threshold_ml(O.code, c, dim, O.table);
         break;
     default: {  // OBJ_TABLE: table[round_half_up(x0)], clamped
         if (lane == 0) {

@@ -348,6 +348,13 @@ def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_t
     fpos = torch.empty((n, cfg.ps, cfg.dim), dtype=torch.float64, device=dev) if want_population else None
     ffit = torch.empty((n, cfg.ps), dtype=torch.float64, device=dev) if want_population else None
     warn = torch.zeros(n, dtype=torch.int64, device=dev)
+    if stream is not None:
+        # inputs were staged on the current stream; the caching allocator must not hand any of these
+        # blocks to other work until the kernel on `stream` is done with them
+        stream.wait_stream(torch.cuda.current_stream())
+        for t in (seeds_t, sched, pdr, best_fit, best_pos, trace, fpos, ffit, warn):
+            if t is not None:
+                t.record_stream(stream)
     t0 = time.perf_counter()
     _lib.check(lib.apo_run_batch(n, _lib.ptr(seeds_t), descs, cfg.ps, cfg.dim, cfg.max_iterations, n_iters,
                                  cfg.neighbor_pairs, cfg.pf_max, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,

@@ -21,7 +21,7 @@ import numpy as np
 
 from .core import ApoConfig
 from .engine import EngineMode, RunResult, run
-from .objectives import Bounds, table_objective
+from .objectives import KAPUR_ML, OTSU_ML, Bounds, Objective, table_objective
 
 
 @dataclass
@@ -137,3 +137,73 @@ def apply_threshold(img: GrayImage, t: int) -> GrayImage:
     if not 0 <= t <= 255:
         raise ValueError(f"t must be in [0, 255], got {t}")
     return GrayImage(np.where(img.pixels > t, 255, 0).astype(np.uint8))
+
+
+# ---------------------------------------------------------------------------
+# Multilevel thresholding (BASELINE config 3; no reference counterpart: the
+# reference stops at one threshold).  Definitions: DESIGN.md and
+# oracle/threshold_oracle.c; k = 1 Otsu reduces to the reference's
+# between_class_variance up to rounding.
+
+METHODS = {"otsu": (0, OTSU_ML), "kapur": (1, KAPUR_ML)}
+TABLE_LEN = 515
+MAX_THRESHOLDS = 32
+
+
+def threshold_tables_device(counts, method: str):
+    """515-entry prefix table (apo_threshold_tables) of a 256-bin histogram -> CUDA tensor."""
+    import torch
+
+    from . import _lib
+
+    if method not in METHODS:
+        raise ValueError(f"method must be one of {tuple(METHODS)}, got {method!r}")
+    lib = _lib.require_cuda()
+    c = counts if isinstance(counts, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(counts, dtype=np.int64))
+    c = c.to(device="cuda", dtype=torch.int64).contiguous()
+    if c.numel() != 256:
+        raise ValueError("counts must have 256 bins")
+    tab = torch.empty(TABLE_LEN, dtype=torch.float64, device=c.device)
+    _lib.check(lib.apo_threshold_tables(_lib.ptr(c), METHODS[method][0], _lib.ptr(tab), _lib.stream_handle()),
+               "apo_threshold_tables")
+    return tab
+
+
+def multilevel_objective(counts, k: int, method: str = "otsu") -> Objective:
+    """Objective over k thresholds in [0, 255]: -(between-class variance) or -(total class entropy)."""
+    if not 1 <= k <= MAX_THRESHOLDS:
+        raise ValueError(f"k must be in [1, {MAX_THRESHOLDS}], got {k}")
+    tab = threshold_tables_device(counts, method).cpu().numpy()
+    return Objective(f"{method}_{k}", METHODS[method][1], min_dim=1, table=tab)
+
+
+class MultiThresholdResult(NamedTuple):
+    thresholds: tuple
+    value: float  # between-class variance (otsu) or total entropy (kapur) at the thresholds
+    run: RunResult
+
+
+def thresholds_of(x) -> tuple:
+    """Sorted integer thresholds the objective reads from a position."""
+    return tuple(sorted(min(max(round_half_up(float(v)), 0), 255) for v in x))
+
+
+def apo_multithreshold(img, k: int, method: str = "otsu", cfg: Optional[ApoConfig] = None, ps: int = 100,
+                       iterations: int = 50, seed: int = 0) -> MultiThresholdResult:
+    """k thresholds maximising Otsu's between-class variance or Kapur's entropy (histogram on the GPU)."""
+    pixels = img.pixels if isinstance(img, GrayImage) else img
+    counts = histogram_device(pixels)
+    obj = multilevel_objective(counts, k, method)
+    box = Bounds(0.0, 255.0, k)
+    cfg = (ApoConfig(ps=ps, dim=k, bounds=box, max_iterations=iterations, seed=seed) if cfg is None
+           else replace(cfg, dim=k, bounds=box))
+    result = run(cfg, obj)
+    return MultiThresholdResult(thresholds_of(result.best_position), -result.best_fitness, result)
+
+
+def multilevel_value(counts, thresholds, method: str = "otsu") -> float:
+    """Objective value (positive) of integer thresholds, evaluated on the device."""
+    from .objectives import evaluate_batch
+
+    obj = multilevel_objective(counts, len(thresholds), method)
+    return -float(evaluate_batch(obj, np.asarray(thresholds, dtype=np.float64)[None, :])[0])

@@ -28,6 +28,8 @@ HGBAT = 3
 ROSENBROCK = 4
 GRIEWANK = 5
 TABLE = 6
+OTSU_ML = 7   # multilevel Otsu over prefix tables (no reference counterpart)
+KAPUR_ML = 8  # multilevel Kapur
 EXTERNAL = -1
 
 
@@ -162,7 +164,7 @@ class DeviceObjective:
         table = None
         if obj.code == HIGH_CONDITIONED_ELLIPTIC:
             table = np.asarray(elliptic_weights(dim))
-        elif obj.code == TABLE:
+        elif obj.code in (TABLE, OTSU_ML, KAPUR_ML):
             table = obj.table
         self.struct = _lib.apo_objective()
         self.struct.code = int(obj.code)
