@@ -35,6 +35,15 @@ extern "C" {
 #define APO_ECUDA 2
 #define APO_ENOMEM 3
 
+/* Random streams (the `rng` argument of the run entry points).
+ * APO_RNG_KEYED: the reference's keyed fmix64 chain (rng.py:79-111) --
+ *   oracle mode, bit-identical to the reference.
+ * APO_RNG_PHILOX: production mode -- Philox4x32-10 keyed by the seed with
+ *   counter (draw slot, protozoon, iteration); same algorithm and slot layout,
+ *   statistically (not bitwise) equivalent. */
+#define APO_RNG_KEYED 0
+#define APO_RNG_PHILOX 1
+
 /* Objective codes (objectives.py:34-42), plus codes the reference lacks. */
 #define APO_OBJ_SPHERE 0
 #define APO_OBJ_BENT_CIGAR 1
@@ -138,7 +147,7 @@ int apo_histogram_u8(const uint8_t *pixels, int64_t n, int64_t *counts, void *st
 typedef struct apo_run apo_run;
 int apo_run_create(apo_run **out, int64_t ps, int64_t dim, int64_t max_iterations, uint64_t seed, int64_t npairs,
                    double pf_max, double lower, double upper, double eps, const apo_objective *objective_host,
-                   const double *sched_host, const double *p_dr_host, void *stream);
+                   const double *sched_host, const double *p_dr_host, int rng, void *stream);
 int apo_run_initialize(apo_run *run);
 /* Runs iterations [t, t+n) where t is the number already run. */
 int apo_run_iterate(apo_run *run, int64_t n);
@@ -175,9 +184,15 @@ int apo_run_batch(int64_t nruns, const uint64_t *seeds, const apo_objective *obj
                   int64_t dim, int64_t max_iterations, int64_t n_iters, int64_t npairs, double pf_max, double lower,
                   double upper, double eps, const double *sched, const double *p_dr, double *best_fit,
                   double *best_pos, double *trace, double *final_pos, double *final_fit, int64_t *warnings,
-                  void *stream);
+                  int rng, void *stream);
 /* Largest ps*dim the batch kernel can hold in shared memory. */
 int64_t apo_run_batch_max_elems(int64_t ps, int64_t dim);
+
+/* Host-side RNG entry points (no device needed; the kernels use the same
+ * code): one Philox4x32-10 block, and the draw u(seed, iteration, individual,
+ * counter) of either stream (rng.py:100-111 for APO_RNG_KEYED). */
+void apo_philox4x32_10(const uint32_t *ctr4, const uint32_t *key2, uint32_t *out4);
+double apo_rng_uniform(int rng, uint64_t seed, uint64_t iteration, uint64_t individual, uint64_t counter);
 
 /* Debug/verification entry: out[k] = device exp_glibc(x[k]). */
 int apo_debug_exp(const double *x, double *out, int64_t n, void *stream);

@@ -113,7 +113,7 @@ PROTOTYPES = {
     "apo_histogram_u8": (_INT, [_P, _I, _P, _P]),
     "apo_threshold_tables": (_INT, [_P, _INT, _P, _P]),
     "apo_run_create": (_INT, [C.POINTER(C.c_void_p), _I, _I, _I, _U, _I, _D, _D, _D, _D, C.POINTER(apo_objective),
-                              _P, _P, _P]),
+                              _P, _P, _INT, _P]),
     "apo_run_initialize": (_INT, [_P]),
     "apo_run_iterate": (_INT, [_P, _I]),
     "apo_run_trace": (_INT, [_P, _P, _I]),
@@ -125,9 +125,11 @@ PROTOTYPES = {
     "apo_run_profile_read": (_INT, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "apo_run_profile_split": (_INT, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "apo_run_batch": (_INT, [_I, _P, C.POINTER(apo_objective), _I, _I, _I, _I, _I, _D, _D, _D, _D, _P, _P, _P, _P,
-                             _P, _P, _P, _P, _P]),
+                             _P, _P, _P, _P, _INT, _P]),
     "apo_run_batch_max_elems": (_I, [_I, _I]),
     "apo_debug_exp": (_INT, [_P, _P, _I, _P]),
+    "apo_philox4x32_10": (None, [_P, _P, _P]),
+    "apo_rng_uniform": (_D, [_INT, _U, _U, _U, _U]),
 }
 
 

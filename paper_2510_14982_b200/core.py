@@ -55,6 +55,9 @@ class ApoConfig:
     max_fes: Optional[int] = None
     seed: int = 0
     eps: float = 2.0 ** -52
+    # "keyed": the reference's fmix64 stream (oracle mode, bit-exact with the reference);
+    # "philox": Philox4x32-10 production stream (same algorithm, statistically equivalent)
+    rng: str = "keyed"
 
     def violations(self) -> list:
         bad = []
@@ -78,6 +81,8 @@ class ApoConfig:
             bad.append(f"seed must be in [0, 2**64), got {self.seed}")
         if not (math.isfinite(self.eps) and self.eps > 0.0):
             bad.append(f"eps must be a positive finite float, got {self.eps}")
+        if self.rng not in ("keyed", "philox"):
+            bad.append(f"rng must be 'keyed' or 'philox', got {self.rng!r}")
         return bad
 
     def __post_init__(self) -> None:

@@ -52,6 +52,88 @@ __host__ __device__ __forceinline__ double uniform(uint64_t base, uint64_t count
 }
 
 // ---------------------------------------------------------------------------
+// Production RNG: Philox4x32-10 (Salmon et al., SC'11), one counter-based
+// stream per (seed, iteration, protozoon): key = seed, counter block =
+// (slot lo, slot hi, protozoon, iteration); the draw is the top 53 bits of
+// the first two output words.  Slots are the reference's draw-slot layout
+// (core.py:18-47), so every draw keeps its meaning; only the bits differ.
+enum RngMode : int { RNG_KEYED = 0, RNG_PHILOX = 1 };
+
+__host__ __device__ __forceinline__ void philox_mulhilo(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
+#ifdef __CUDA_ARCH__
+    hi = __umulhi(a, b);
+    lo = a * b;
+#else
+    const uint64_t p = (uint64_t)a * (uint64_t)b;
+    hi = (uint32_t)(p >> 32);
+    lo = (uint32_t)p;
+#endif
+}
+
+__host__ __device__ inline void philox4x32_10_block(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        uint32_t hi0, lo0, hi1, lo1;
+        philox_mulhilo(0xD2511F53u, c[0], hi0, lo0);
+        philox_mulhilo(0xCD9E8D57u, c[2], hi1, lo1);
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = lo1;
+        c[2] = n2;
+        c[3] = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+__host__ __device__ inline uint64_t philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                                  uint32_t k1) {
+    uint32_t c[4] = {c0, c1, c2, c3};
+    philox4x32_10_block(c, k0, k1);
+    return ((uint64_t)c[0] << 32) | c[1];
+}
+
+// Per-protozoon stream key for either generator.  uniform(Key, counter) is
+// the only draw primitive the kernels use.
+struct Key {
+    uint64_t a;   // keyed: the fmix64 stream base; philox: the seed
+    uint32_t b;   // philox: protozoon (folded to 32 bits; the coordinator maps above 2^31)
+    uint32_t c;   // philox: iteration
+    int mode;
+};
+
+__host__ __device__ __forceinline__ Key stream_key(int mode, uint64_t seed, uint64_t iteration, uint64_t individual) {
+    Key k;
+    k.mode = mode;
+    if (mode == RNG_PHILOX) {
+        k.a = seed;
+        k.b = (uint32_t)individual ^ ((uint32_t)(individual >> 32) * 0x9E3779B9u);
+        k.c = (uint32_t)iteration;
+    } else {
+        k.a = stream_base(seed, iteration, individual);
+        k.b = k.c = 0;
+    }
+    return k;
+}
+
+#ifdef __CUDA_ARCH__
+__device__ __noinline__ double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
+    return (double)(philox4x32_10((uint32_t)counter, (uint32_t)(counter >> 32), b, c, (uint32_t)seed,
+                                  (uint32_t)(seed >> 32)) >> 11) * kInv2p53;
+}
+#else
+inline double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
+    return (double)(philox4x32_10((uint32_t)counter, (uint32_t)(counter >> 32), b, c, (uint32_t)seed,
+                                  (uint32_t)(seed >> 32)) >> 11) * kInv2p53;
+}
+#endif
+
+__host__ __device__ __forceinline__ double uniform(const Key& k, uint64_t counter) {
+    if (k.mode == RNG_PHILOX) return philox_uniform(k.a, k.b, k.c, counter);
+    return uniform(k.a, counter);
+}
+
+// ---------------------------------------------------------------------------
 // glibc exp (sysdeps/ieee754/dbl-64/e_exp.c algorithm, FMA build).
 
 #define APO_EXP_TABLE { \

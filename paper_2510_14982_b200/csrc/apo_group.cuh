@@ -235,7 +235,7 @@ template <class Rows>
 __device__ inline void group_phase_a(const IterParams& P, const Rows& R, int i, bool in_dr, double p_dr_i,
                                      const GroupScratch& g, int lane) {
     const int ps = P.ps, dim = P.dim;
-    const uint64_t base = stream_base(P.seed, P.key_iteration, (uint64_t)i);
+    const Key base = stream_key(P.rng, P.seed, P.key_iteration, (uint64_t)i);
     const double u_dec = uniform(base, kSlotDecision);
     int op;
     if (in_dr) op = (u_dec < p_dr_i) ? OP_DORMANCY : OP_REPRODUCTION;
@@ -308,7 +308,7 @@ __device__ __forceinline__ double gmask(const GroupScratch& g, int p, int d) {
 
 // Pairs k >= 1 when npairs > 1 (warp-parallel, cached in g.ws.pk / g.ws.pw).
 template <class Rows>
-__device__ inline void group_extra_pairs(const IterParams& P, const Rows& R, int i, int op, uint64_t base,
+__device__ inline void group_extra_pairs(const IterParams& P, const Rows& R, int i, int op, const Key& base,
                                          const GroupScratch& g, int lane) {
     const int ps = P.ps;
     if (lane >= 1 && lane < kMaxCachedPairs && lane < P.npairs) {
@@ -343,7 +343,7 @@ __device__ inline void group_extra_pairs(const IterParams& P, const Rows& R, int
 // acc for pairs k >= 1 at dimension d (pair 0 is added by the caller first,
 // so the accumulation order matches the reference: acc = 0; acc += w_k*(...)).
 template <class Rows>
-__device__ __forceinline__ double extra_pairs_acc(const IterParams& P, const Rows& R, int i, int op, uint64_t base,
+__device__ __forceinline__ double extra_pairs_acc(const IterParams& P, const Rows& R, int i, int op, const Key& base,
                                                   const GroupScratch& g, double acc, int d) {
     for (int k = 1; k < P.npairs; k++) {
         int skm, skp;
@@ -499,8 +499,8 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
     const double* x = staged ? staged : R.at_key(sl[0]);
     const double f = g.f[p];
     const bool many = MANY && op >= OP_AUTOTROPH;
-    uint64_t base = 0;
-    if (op != OP_AUTOTROPH || many) base = stream_base(P.seed, P.key_iteration, (uint64_t)i);
+    Key base{};
+    if (op != OP_AUTOTROPH || many) base = stream_key(P.rng, P.seed, P.key_iteration, (uint64_t)i);
     if (many) group_extra_pairs(P, R, i, op, base, g, lane);
     const double* xj = staged ? staged + g.rld : R.at_key(sl[op == OP_AUTOTROPH ? 1 : 0]);
     const double* xm = staged ? staged + 2 * g.rld : R.at_key(sl[op >= OP_AUTOTROPH ? 2 : 0]);

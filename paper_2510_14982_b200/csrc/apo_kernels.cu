@@ -111,7 +111,7 @@ int check_objective(const apo_objective* o, int64_t dim) {
 
 
 
-__global__ void __launch_bounds__(kThreads) k_init(uint64_t seed, int ps, int dim, int ld, double lower,
+__global__ void __launch_bounds__(kThreads) k_init(int rng, uint64_t seed, int ps, int dim, int ld, double lower,
                                                    double span, ObjDesc O, double* __restrict__ pos,
                                                    double* __restrict__ fit, unsigned long long* trace_key) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreads) k_init(uint64_t seed, int ps, int di
     const WarpScratch s = warp_scratch(smem + (size_t)warp * warp_scratch_bytes(dim), dim);
     unsigned long long my_min = ~0ull;
     for (int r0 = blockIdx.x * nwarps + warp; r0 < ps; r0 += gridDim.x * nwarps) {
-        const uint64_t base = stream_base(seed, 0, (uint64_t)(r0 + 1));
+        const Key base = stream_key(rng, seed, 0, (uint64_t)(r0 + 1));
         double* row = pos + (size_t)r0 * ld;
         for (int d = lane; d < dim; d += 32) {
             const double c = lower + uniform(base, (uint64_t)d) * span;
@@ -173,7 +173,7 @@ __global__ void k_iota(int n, int* __restrict__ v) {
 // counters 1.., core.py:271-278).  Step j's target r_j is packed with j so a
 // radix sort groups same-target steps in step order; resolution then walks
 // "latest earlier step with the same target" by binary search.
-__global__ void k_dr_draw(int count, int n, uint64_t base, unsigned long long* __restrict__ keys) {
+__global__ void k_dr_draw(int count, int n, Key base, unsigned long long* __restrict__ keys) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
         const double u = uniform(base, 1ull + (uint64_t)j);
         int r = j + (int)(u * (double)(n - j));
@@ -196,7 +196,7 @@ __device__ __forceinline__ int latest_before(const unsigned long long* keys, int
     return (int)(keys[q] & 0xFFFFFFFFull);
 }
 
-__global__ void k_dr_resolve(int count, int n, uint64_t base, const unsigned long long* __restrict__ keys,
+__global__ void k_dr_resolve(int count, int n, Key base, const unsigned long long* __restrict__ keys,
                              unsigned* __restrict__ bits, uint8_t* __restrict__ bytes) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
         const double u = uniform(base, 1ull + (uint64_t)j);
@@ -367,20 +367,20 @@ int nbits_for(long long n) {
     return b;
 }
 
-uint64_t coord_count(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_max) {
-    const uint64_t cbase = stream_base(seed, key_iteration, kCoordinator);
+uint64_t coord_count(int rng, uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_max) {
+    const Key cbase = stream_key(rng, seed, key_iteration, kCoordinator);
     const double pf = pf_max * uniform(cbase, 0);
     return (uint64_t)ceil((double)ps * pf);
 }
 
 // Coordinator Dr on device given scratch (keys + sorted keys + CUB temp).
-int dr_device(uint64_t seed, uint64_t key_iteration, int64_t ps, int64_t count, unsigned long long* keys,
+int dr_device(int rng, uint64_t seed, uint64_t key_iteration, int64_t ps, int64_t count, unsigned long long* keys,
               unsigned long long* keys_sorted, void* tmp, size_t tmp_bytes, unsigned* bits, uint8_t* bytes,
               cudaStream_t st) {
     if (bits) APO_CUDA(cudaMemsetAsync(bits, 0, 4 * (size_t)((ps + 31) / 32), st));
     if (bytes) APO_CUDA(cudaMemsetAsync(bytes, 0, (size_t)ps, st));
     if (count <= 0) return APO_OK;
-    const uint64_t cbase = stream_base(seed, key_iteration, kCoordinator);
+    const Key cbase = stream_key(rng, seed, key_iteration, kCoordinator);
     k_dr_draw<<<grid_for(count, 256), 256, 0, st>>>((int)count, (int)ps, cbase, keys);
     APO_CUDA(cudaGetLastError());
     size_t bytes_needed = tmp_bytes;
@@ -406,6 +406,7 @@ size_t dr_tmp_bytes(int64_t cap, int64_t ps) {
 
 struct apo_run {
     int64_t ps, dim, ld, T;
+    int rng;  // RngMode
     uint64_t seed;
     int64_t npairs;
     double pf_max, lower, upper, eps;
@@ -474,6 +475,7 @@ int apo_run_updates_obj(const double* positions, const double* fitness, const ui
     P.p_ah = p_ah;
     P.f_mult = f_mult;
     P.decay = decay;
+    P.rng = RNG_KEYED;  // the reference-facing boundary is always oracle mode
     if (warn_count) APO_CUDA(cudaMemsetAsync(warn_count, 0, sizeof(unsigned long long), as_stream(stream)));
     UpdArgs A{};
     A.P = P;
@@ -538,7 +540,7 @@ int apo_initialize(uint64_t seed, int64_t ps, int64_t dim, int64_t ld, double lo
     const long long need = (ps + w - 1) / w;
     const long long cap = 8LL * num_sms();
     k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, as_stream(stream)>>>(
-        seed, (int)ps, (int)dim, (int)ld, lower, span, to_desc(objective_host), positions, fitness, nullptr);
+        RNG_KEYED, seed, (int)ps, (int)dim, (int)ld, lower, span, to_desc(objective_host), positions, fitness, nullptr);
     APO_CUDA(cudaGetLastError());
     return APO_OK;
 }
@@ -571,7 +573,7 @@ int apo_select_dr(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_m
     APO_CHECK(ps >= 1 && ps < (1LL << 31) && in_dr, "bad arguments");
     APO_CHECK(pf_max > 0.0 && pf_max <= 1.0, "pf_max must be in (0, 1]");
     cudaStream_t st = as_stream(stream);
-    const int64_t count = (int64_t)coord_count(seed, key_iteration, ps, pf_max);
+    const int64_t count = (int64_t)coord_count(RNG_KEYED, seed, key_iteration, ps, pf_max);
     if (count_host) *count_host = count;
     unsigned long long *keys = nullptr, *sorted = nullptr;
     void* tmp = nullptr;
@@ -581,7 +583,7 @@ int apo_select_dr(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_m
         APO_CUDA(cudaMallocAsync((void**)&sorted, 8 * (size_t)count, st));
         APO_CUDA(cudaMallocAsync(&tmp, tb, st));
     }
-    int rc = dr_device(seed, key_iteration, ps, count, keys, sorted, tmp, tb, nullptr, in_dr, st);
+    int rc = dr_device(RNG_KEYED, seed, key_iteration, ps, count, keys, sorted, tmp, tb, nullptr, in_dr, st);
     if (count > 0) {
         cudaFreeAsync(keys, st);
         cudaFreeAsync(sorted, st);
@@ -611,6 +613,16 @@ int apo_threshold_tables(const int64_t* counts, int method, double* table, void*
     return APO_OK;
 }
 
+void apo_philox4x32_10(const uint32_t* ctr4, const uint32_t* key2, uint32_t* out4) {
+    uint32_t c[4] = {ctr4[0], ctr4[1], ctr4[2], ctr4[3]};
+    philox4x32_10_block(c, key2[0], key2[1]);
+    for (int k = 0; k < 4; k++) out4[k] = c[k];
+}
+
+double apo_rng_uniform(int rng, uint64_t seed, uint64_t iteration, uint64_t individual, uint64_t counter) {
+    return uniform(stream_key(rng, seed, iteration, individual), counter);
+}
+
 int apo_debug_exp(const double* x, double* out, int64_t n, void* stream) {
     APO_CHECK(n >= 0, "bad n");
     if (n == 0) return APO_OK;
@@ -623,7 +635,8 @@ int apo_debug_exp(const double* x, double* out, int64_t n, void* stream) {
 
 int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iterations, uint64_t seed, int64_t npairs,
                    double pf_max, double lower, double upper, double eps, const apo_objective* objective_host,
-                   const double* sched_host, const double* p_dr_host, void* stream) {
+                   const double* sched_host, const double* p_dr_host, int rng, void* stream) {
+    APO_CHECK(rng == RNG_KEYED || rng == RNG_PHILOX, "rng must be APO_RNG_KEYED or APO_RNG_PHILOX");
     APO_CHECK(out != nullptr, "out is NULL");
     APO_CHECK(ps >= 1 && ps < (1LL << 31) && dim >= 1 && dim <= 8192, "bad shape");
     APO_CHECK(max_iterations >= 0 && npairs >= 1 && pf_max > 0.0 && pf_max <= 1.0, "bad config");
@@ -633,6 +646,7 @@ int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iteration
     apo_run* r = new apo_run();
     r->ps = ps;
     r->dim = dim;
+    r->rng = rng;
     r->ld = (dim + 1) & ~1LL;  // 16-byte aligned rows
     r->T = max_iterations;
     r->seed = seed;
@@ -701,7 +715,7 @@ int apo_run_initialize(apo_run* r) {
     const long long cap = (long long)(per_sm > 0 ? per_sm : 1) * num_sms();
     APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(r->T + 1), st));
     APO_CUDA(cudaMemsetAsync(r->warn, 0, 8, st));
-    k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, st>>>(r->seed, (int)r->ps, (int)r->dim, (int)r->ld,
+    k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, st>>>(r->rng, r->seed, (int)r->ps, (int)r->dim, (int)r->ld,
                                                                   r->lower, r->upper - r->lower, r->obj, r->pos[0],
                                                                   r->fit[0], r->trace_keys);
     APO_CUDA(cudaGetLastError());
@@ -729,8 +743,8 @@ int apo_run_iterate(apo_run* r, int64_t n) {
         APO_CUDA(cub::DeviceRadixSort::SortPairs(r->tmp, tb, r->keys_in, r->keys_out, r->vals_in, r->order, ps, 0, 64,
                                                  st));
         // 2. coordinator draws
-        const int64_t count = (int64_t)coord_count(r->seed, key_it, r->ps, r->pf_max);
-        if (int rc = dr_device(r->seed, key_it, r->ps, count, r->dr_keys, r->dr_sorted, r->tmp, r->tmp_bytes,
+        const int64_t count = (int64_t)coord_count(r->rng, r->seed, key_it, r->ps, r->pf_max);
+        if (int rc = dr_device(r->rng, r->seed, key_it, r->ps, count, r->dr_keys, r->dr_sorted, r->tmp, r->tmp_bytes,
                                r->dr_bits, nullptr, st))
             return rc;
         // 3. fused update
@@ -748,6 +762,7 @@ int apo_run_iterate(apo_run* r, int64_t n) {
         P.p_ah = r->sched[3 * t];
         P.f_mult = r->sched[3 * t + 1];
         P.decay = r->sched[3 * t + 2];
+        P.rng = r->rng;
         cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
         if (r->profile) {
             for (auto& e : ev) {
@@ -911,7 +926,8 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
                   int64_t dim, int64_t max_iterations, int64_t n_iters, int64_t npairs, double pf_max, double lower,
                   double upper, double eps, const double* sched, const double* p_dr, double* best_fit,
                   double* best_pos, double* trace, double* final_pos, double* final_fit, int64_t* warnings,
-                  void* stream) {
+                  int rng, void* stream) {
+    APO_CHECK(rng == RNG_KEYED || rng == RNG_PHILOX, "rng must be APO_RNG_KEYED or APO_RNG_PHILOX");
     APO_CHECK(nruns >= 1 && nruns < (1LL << 31), "nruns out of range");
     APO_CHECK(ps >= 1 && dim >= 1 && dim <= 8192, "bad shape");
     APO_CHECK(n_iters >= 0 && n_iters <= max_iterations, "n_iters must be in [0, max_iterations]");
@@ -948,6 +964,7 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     A.final_pos = final_pos;
     A.final_fit = final_fit;
     A.warnings = (long long*)warnings;
+    A.rng = rng;
     A.cec_bufs = 0;
     A.tab_smem = 0;
     for (int64_t k = 0; k < nruns; k++) {

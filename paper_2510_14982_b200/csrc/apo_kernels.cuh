@@ -166,6 +166,7 @@ struct BatchArgs {
     long long* warnings;
     int cec_bufs;   // max over the batch's objectives of cec_bufs_for(code)
     int tab_smem;   // doubles of threshold prefix table staged in shared memory (0 = none)
+    int rng;        // RngMode
 };
 
 struct BatchLayout {
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
     unsigned long long my_min = ~0ull;
     const WarpScratch iws = warp_scratch(wbase, dim);
     for (int r0 = warp; r0 < ps; r0 += nwarps) {
-        const uint64_t base = stream_base(seed, 0, (uint64_t)(r0 + 1));
+        const Key base = stream_key(A.rng, seed, 0, (uint64_t)(r0 + 1));
         double* row = pos[0] + (size_t)r0 * ld;
         for (int d = lane; d < dim; d += 32) row[d] = A.lower + uniform(base, (uint64_t)d) * A.span;
         __syncwarp();
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
         // 2. coordinator draws (core.py:263-278)
         const uint64_t key_it = (uint64_t)t + 1;
         if (warp == 0) {
-            const uint64_t cbase = stream_base(seed, key_it, kCoordinator);
+            const Key cbase = stream_key(A.rng, seed, key_it, kCoordinator);
             const double pf = A.pf_max * uniform(cbase, 0);
             const int count = (int)ceil((double)ps * pf);
             build_mask(ps, count, cbase, 1, cs, lane);
@@ -311,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
         P.p_ah = A.sched[3 * t];
         P.f_mult = A.sched[3 * t + 1];
         P.decay = A.sched[3 * t + 2];
+        P.rng = A.rng;
         const int nxt = cur ^ 1;
         my_min = ~0ull;
         unsigned my_warn = 0;

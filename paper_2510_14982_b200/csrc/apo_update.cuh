@@ -31,6 +31,7 @@ struct IterParams {
     int ld;  // row stride (doubles) of the source/target population
     double lower, upper, span, eps;
     double p_ah, f_mult, decay;
+    int rng;  // RngMode: RNG_KEYED (reference fmix64, oracle mode) or RNG_PHILOX (production)
 };
 
 // Per-warp shared-memory scratch (carved by warp_scratch()).
@@ -84,7 +85,7 @@ __device__ inline WarpScratch warp_scratch(unsigned char* base, int dim) {
 // which is exactly mask[perm[j]-1] = 1 in the reference.
 // If `sel` is non-null the selected 0-based values are also written there in
 // slot order (the coordinator's Dr list needs them; the mask does not).
-__device__ inline void build_mask(int n, int count, uint64_t base, uint64_t ctr0, const WarpScratch& s, int lane) {
+__device__ inline void build_mask(int n, int count, const Key& base, uint64_t ctr0, const WarpScratch& s, int lane) {
     const int words = (n + 31) >> 5;
     for (int p = lane; p < n; p += 32) s.head[p] = -1;
     for (int w = lane; w < words; w += 32) s.bits[w] = 0u;
@@ -168,7 +169,7 @@ __device__ inline UpdateResult update_protozoon(const IterParams& P, const ObjDe
     const int ps = P.ps, dim = P.dim;
     const double* x = R.row(i);
     const double fit_i = R.fitness(i);
-    const uint64_t base = stream_base(P.seed, P.key_iteration, (uint64_t)i);
+    const Key base = stream_key(P.rng, P.seed, P.key_iteration, (uint64_t)i);
     const double u_dec = uniform(base, kSlotDecision);
 
     int op;

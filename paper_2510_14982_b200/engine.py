@@ -162,6 +162,9 @@ def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: Engin
                          f"(ps={cfg.ps}, dim={cfg.dim})")
     bk = _resolve_backend(obj, backend)
     workers = resolve_workers(mode, bk)
+    if cfg.rng != "keyed":
+        raise ValueError("step() is the reference-facing per-iteration path and uses the reference's keyed "
+                         "stream; Philox production mode runs through run()/run_batch()/DeviceRun")
     lib = _lib.require_cuda()
     dev = _dev()
     stream = _lib.stream_handle()
@@ -203,7 +206,7 @@ class DeviceRun:
         _lib.check(self.lib.apo_run_create(C.byref(h), cfg.ps, cfg.dim, cfg.max_iterations, cfg.seed,
                                            cfg.neighbor_pairs, cfg.pf_max, cfg.bounds.lower, cfg.bounds.upper,
                                            cfg.eps, self.dobj.ref, sched.ctypes.data, pdr.ctypes.data,
-                                           _lib.stream_handle(stream)), "apo_run_create")
+                                           rng_code(cfg), _lib.stream_handle(stream)), "apo_run_create")
         self.handle = h
         self._torch = torch
 
@@ -263,6 +266,11 @@ class DeviceRun:
             self.close()
         except Exception:
             pass
+
+
+def rng_code(cfg: ApoConfig) -> int:
+    """APO_RNG_KEYED (0, reference stream, oracle mode) or APO_RNG_PHILOX (1, production)."""
+    return 1 if cfg.rng == "philox" else 0
 
 
 def _batch_fits(cfg: ApoConfig) -> bool:
@@ -360,7 +368,7 @@ def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_t
                                  cfg.neighbor_pairs, cfg.pf_max, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,
                                  _lib.ptr(sched), _lib.ptr(pdr), _lib.ptr(best_fit), _lib.ptr(best_pos),
                                  _lib.ptr(trace), _lib.ptr(fpos), _lib.ptr(ffit), _lib.ptr(warn),
-                                 _lib.stream_handle(stream)), "apo_run_batch")
+                                 rng_code(cfg), _lib.stream_handle(stream)), "apo_run_batch")
     if device_out:
         return BatchResult(best_fit, best_pos, trace, warn, fpos, ffit, 0.0, tuple(o.name for o in objs),
                            tuple(seeds))
