@@ -171,6 +171,34 @@ int apo_run_profile_read(apo_run *run, double *update_ms_host, int64_t *launches
 int apo_run_profile_split(apo_run *run, double *candidates_ms_host, double *evaluate_ms_host, int64_t *launches_host);
 
 /*
+ * One population sharded by rank across processes (engine.run with the
+ * population split over N GPUs, BASELINE config 4).  Each process keeps the
+ * whole population in rank order of the previous iteration in caller-owned
+ * buffers pos0/pos1 [ps_pad][ld] and fit0/fit1 [ps_pad]; per iteration:
+ *   apo_shard_begin          stable sort + coordinator draws (replicated)
+ *   apo_shard_update_range   update ranks [lo, hi) into the next buffers
+ *   (caller)                 all-gather rows [lo, hi) of the next buffers
+ *   apo_shard_end            the next buffers become current
+ * Results are identical for every partition (tests/test_shard.py).
+ * trace keys / warnings count this process's ranks only: reduce them
+ * (MIN / SUM) across processes.  dim <= 256.
+ */
+typedef struct apo_shard apo_shard;
+int apo_shard_create(apo_shard **out, int64_t ps, int64_t dim, int64_t ld, int64_t max_iterations, uint64_t seed,
+                     int64_t npairs, double pf_max, double lower, double upper, double eps,
+                     const apo_objective *objective_host, const double *sched_host, const double *p_dr_host, int rng,
+                     double *pos0, double *pos1, double *fit0, double *fit1, void *stream);
+int apo_shard_initialize(apo_shard *shard);
+int apo_shard_begin(apo_shard *shard);
+int apo_shard_update_range(apo_shard *shard, int64_t lo, int64_t hi);
+int apo_shard_end(apo_shard *shard);
+/* Device pointers of the current buffers and the iterations run. */
+int apo_shard_state(apo_shard *shard, double **pos_dev, double **fit_dev, int64_t *iterations_host);
+/* Order-preserving trace keys (entries 0..n; decode like apo_run_trace) and warnings of this process. */
+int apo_shard_counters(apo_shard *shard, unsigned long long *trace_keys_host, int64_t n, int64_t *warnings_host);
+int apo_shard_destroy(apo_shard *shard);
+
+/*
  * Many independent small runs, one CTA per run, the whole run resident in
  * shared memory for all iterations (BASELINE configs 1-3 and 5: seeds x
  * objectives).  objectives_host: nruns descriptors; seeds: device [nruns].

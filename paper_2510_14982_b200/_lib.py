@@ -127,6 +127,15 @@ PROTOTYPES = {
     "apo_run_batch": (_INT, [_I, _P, C.POINTER(apo_objective), _I, _I, _I, _I, _I, _D, _D, _D, _D, _P, _P, _P, _P,
                              _P, _P, _P, _P, _INT, _P]),
     "apo_run_batch_max_elems": (_I, [_I, _I]),
+    "apo_shard_create": (_INT, [C.POINTER(C.c_void_p), _I, _I, _I, _I, _U, _I, _D, _D, _D, _D,
+                                C.POINTER(apo_objective), _P, _P, _INT, _P, _P, _P, _P, _P]),
+    "apo_shard_initialize": (_INT, [_P]),
+    "apo_shard_begin": (_INT, [_P]),
+    "apo_shard_update_range": (_INT, [_P, _I, _I]),
+    "apo_shard_end": (_INT, [_P]),
+    "apo_shard_state": (_INT, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "apo_shard_counters": (_INT, [_P, _P, _I, C.POINTER(C.c_int64)]),
+    "apo_shard_destroy": (_INT, [_P]),
     "apo_debug_exp": (_INT, [_P, _P, _I, _P]),
     "apo_philox4x32_10": (None, [_P, _P, _P]),
     "apo_rng_uniform": (_D, [_INT, _U, _U, _U, _U]),

@@ -310,7 +310,8 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
     if (per_sm < 1) per_sm = 1;
-    const long long units = group ? ((long long)a.P.ps + 31) / 32 : (long long)a.P.ps;
+    if (a.rank_hi <= 0) a.rank_hi = a.P.ps;  // default: every rank
+    const long long units = group ? ((long long)(a.rank_hi - a.rank_lo) + 31) / 32 : (long long)a.P.ps;
     const long long need = (units + w - 1) / w;
     const long long cap = (long long)per_sm * num_sms();
     const int grid = (int)(need < cap ? need : cap);
@@ -321,7 +322,9 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     if (mid_event) APO_CUDA(cudaEventRecord(mid_event, st));
     if (!split) return APO_OK;
     CecEvalArgs E{};
-    E.n_rows = a.P.ps;
+    E.row0 = a.rank_lo;
+    E.n_rows = a.rank_hi - a.rank_lo;
+    E.order = sel_mode ? nullptr : a.order;
     E.dim = dim;
     E.ld = a.P.ld;
     E.O = a.O;
@@ -905,6 +908,215 @@ int apo_run_destroy(apo_run* r) {
     clear_profile(r);
     void* bufs[] = {r->pos[0], r->pos[1], r->sel[0], r->sel[1], r->fit[0], r->fit[1], r->order, r->keys_in, r->keys_out, r->vals_in,
                     r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn, r->cand_ok};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    delete r;
+    return APO_OK;
+}
+
+// ----------------------------- sharded population -----------------------------
+// One huge population split by RANK across processes (BASELINE config 4 on N
+// GPUs).  Every process holds the whole population in rank order of the
+// previous iteration (rows = "slots"), computes the identical stable sort
+// and Dr set, updates only ranks [lo, hi) into the next buffer (rows by
+// rank), and the caller exchanges the chunks (NCCL all-gather over NVLink)
+// before apo_shard_end.  Position/fitness buffers are the caller's
+// (torch tensors registered with NCCL), [ps_pad][ld] and [ps_pad].
+struct apo_shard {
+    int64_t ps, dim, ld, T;
+    int rng;
+    uint64_t seed;
+    int64_t npairs;
+    double pf_max, lower, upper, eps;
+    ObjDesc obj;
+    cudaStream_t stream;
+    double* pos[2];
+    double* fit[2];
+    int cur;
+    int* order;
+    unsigned long long *keys_in, *keys_out, *dr_keys, *dr_sorted;
+    int* vals_in;
+    unsigned* dr_bits;
+    int64_t dr_cap;
+    void* tmp;
+    size_t tmp_bytes;
+    double* p_dr;
+    uint8_t* cand_ok;
+    unsigned long long* trace_keys;  // [T+1], this process's ranks only (reduce MIN across processes)
+    unsigned long long* warn;        // this process's ranks only (reduce SUM)
+    std::vector<double> sched;
+    int64_t iters;
+};
+
+int apo_shard_create(apo_shard** out, int64_t ps, int64_t dim, int64_t ld, int64_t max_iterations, uint64_t seed,
+                     int64_t npairs, double pf_max, double lower, double upper, double eps,
+                     const apo_objective* objective_host, const double* sched_host, const double* p_dr_host, int rng,
+                     double* pos0, double* pos1, double* fit0, double* fit1, void* stream) {
+    APO_CHECK(out != nullptr, "out is NULL");
+    APO_CHECK(ps >= 1 && ps < (1LL << 31) && dim >= 1 && dim <= kGroupMaxDim && ld >= dim,
+              "sharded runs need 1 <= dim <= 256 and ld >= dim");
+    APO_CHECK(max_iterations >= 0 && npairs >= 1 && pf_max > 0.0 && pf_max <= 1.0, "bad config");
+    APO_CHECK(rng == RNG_KEYED || rng == RNG_PHILOX, "bad rng");
+    APO_CHECK((max_iterations == 0 || sched_host) && p_dr_host && pos0 && pos1 && fit0 && fit1, "NULL buffer");
+    if (int rc = check_objective(objective_host, dim)) return rc;
+    apo_shard* r = new apo_shard();
+    r->ps = ps;
+    r->dim = dim;
+    r->ld = ld;
+    r->T = max_iterations;
+    r->rng = rng;
+    r->seed = seed;
+    r->npairs = npairs;
+    r->pf_max = pf_max;
+    r->lower = lower;
+    r->upper = upper;
+    r->eps = eps;
+    r->obj = to_desc(objective_host);
+    r->stream = as_stream(stream);
+    r->pos[0] = pos0;
+    r->pos[1] = pos1;
+    r->fit[0] = fit0;
+    r->fit[1] = fit1;
+    r->cur = 0;
+    r->iters = 0;
+    r->sched.assign(sched_host, sched_host + 3 * max_iterations);
+    r->dr_cap = (int64_t)ceil((double)ps * pf_max) + 1;
+    size_t tb_sort = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (int*)nullptr, (int*)nullptr, (int)ps, 0, 64, r->stream);
+    const size_t tb_dr = dr_tmp_bytes(r->dr_cap, ps);
+    r->tmp_bytes = tb_sort > tb_dr ? tb_sort : tb_dr;
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](void** p, size_t b) {
+        if (e == cudaSuccess) e = cudaMalloc(p, b > 0 ? b : 16);
+    };
+    alloc((void**)&r->order, 4 * (size_t)ps);
+    alloc((void**)&r->keys_in, 8 * (size_t)ps);
+    alloc((void**)&r->keys_out, 8 * (size_t)ps);
+    alloc((void**)&r->vals_in, 4 * (size_t)ps);
+    alloc((void**)&r->dr_keys, 8 * (size_t)r->dr_cap);
+    alloc((void**)&r->dr_sorted, 8 * (size_t)r->dr_cap);
+    alloc((void**)&r->dr_bits, 4 * (size_t)((ps + 31) / 32));
+    alloc(&r->tmp, r->tmp_bytes);
+    alloc((void**)&r->p_dr, 8 * (size_t)ps);
+    alloc((void**)&r->cand_ok, (size_t)ps);
+    alloc((void**)&r->trace_keys, 8 * (size_t)(max_iterations + 1));
+    alloc((void**)&r->warn, 8);
+    if (e != cudaSuccess) {
+        apo_shard_destroy(r);
+        return fail(APO_ENOMEM, std::string("apo_shard_create: ") + cudaGetErrorString(e));
+    }
+    APO_CUDA(cudaMemcpyAsync(r->p_dr, p_dr_host, 8 * (size_t)ps, cudaMemcpyHostToDevice, r->stream));
+    APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(max_iterations + 1), r->stream));
+    APO_CUDA(cudaMemsetAsync(r->warn, 0, 8, r->stream));
+    *out = r;
+    return APO_OK;
+}
+
+int apo_shard_initialize(apo_shard* r) {
+    APO_CHECK(r, "shard is NULL");
+    cudaStream_t st = r->stream;
+    const int w = warps_for_dim(r->dim);
+    const size_t smem = warp_scratch_bytes((int)r->dim) * (size_t)w;
+    if (int rc = set_smem((const void*)k_init, smem)) return rc;
+    const long long need = (r->ps + w - 1) / w;
+    const long long cap = 8LL * num_sms();
+    APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(r->T + 1), st));
+    APO_CUDA(cudaMemsetAsync(r->warn, 0, 8, st));
+    // every process builds the identical iteration-0 population (replicated, no exchange)
+    k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, st>>>(r->rng, r->seed, (int)r->ps, (int)r->dim, (int)r->ld,
+                                                                  r->lower, r->upper - r->lower, r->obj, r->pos[0],
+                                                                  r->fit[0], r->trace_keys);
+    APO_CUDA(cudaGetLastError());
+    r->cur = 0;
+    r->iters = 0;
+    return APO_OK;
+}
+
+// Sort + coordinator draws of the next iteration (identical on every process).
+int apo_shard_begin(apo_shard* r) {
+    APO_CHECK(r && r->iters < r->T, "iteration budget exceeded");
+    cudaStream_t st = r->stream;
+    const int ps = (int)r->ps;
+    const uint64_t key_it = (uint64_t)r->iters + 1;
+    // rows are in rank order of the previous iteration, so ties keep row order
+    k_make_keys<<<grid_for(ps, 256), 256, 0, st>>>(ps, r->fit[r->cur], nullptr, r->keys_in, r->vals_in);
+    APO_CUDA(cudaGetLastError());
+    size_t tb = r->tmp_bytes;
+    APO_CUDA(cub::DeviceRadixSort::SortPairs(r->tmp, tb, r->keys_in, r->keys_out, r->vals_in, r->order, ps, 0, 64, st));
+    const int64_t count = (int64_t)coord_count(r->rng, r->seed, key_it, r->ps, r->pf_max);
+    return dr_device(r->rng, r->seed, key_it, r->ps, count, r->dr_keys, r->dr_sorted, r->tmp, r->tmp_bytes, r->dr_bits,
+                     nullptr, st);
+}
+
+// Update ranks [lo, hi) (lo % 32 == 0) into the next buffers (rows by rank).
+int apo_shard_update_range(apo_shard* r, int64_t lo, int64_t hi) {
+    APO_CHECK(r && lo >= 0 && lo <= hi && hi <= r->ps, "bad rank range");
+    if (hi == lo) return APO_OK;
+    APO_CHECK((lo & 31) == 0, "rank ranges must start on a multiple of 32");
+    const int64_t t = r->iters;
+    UpdArgs A{};
+    A.P.seed = r->seed;
+    A.P.key_iteration = (uint64_t)t + 1;
+    A.P.ps = (int)r->ps;
+    A.P.dim = (int)r->dim;
+    A.P.npairs = (int)r->npairs;
+    A.P.ld = (int)r->ld;
+    A.P.lower = r->lower;
+    A.P.upper = r->upper;
+    A.P.span = r->upper - r->lower;
+    A.P.eps = r->eps;
+    A.P.p_ah = r->sched[3 * t];
+    A.P.f_mult = r->sched[3 * t + 1];
+    A.P.decay = r->sched[3 * t + 2];
+    A.P.rng = r->rng;
+    A.O = r->obj;
+    A.pos = r->pos[r->cur];
+    A.fit = r->fit[r->cur];
+    A.order = r->order;
+    A.out_pos = r->pos[r->cur ^ 1];
+    A.out_fit = r->fit[r->cur ^ 1];
+    A.in_dr_bits = r->dr_bits;
+    A.p_dr = r->p_dr;
+    A.warn_count = r->warn;
+    A.trace_key = r->trace_keys + t + 1;
+    A.cec_bufs = cec_bufs_for(r->obj.code);
+    A.rank_lo = (int)lo;
+    A.rank_hi = (int)hi;
+    return launch_update(false, A, r->stream, r->cand_ok);
+}
+
+int apo_shard_end(apo_shard* r) {
+    APO_CHECK(r, "shard is NULL");
+    r->cur ^= 1;
+    r->iters++;
+    return APO_OK;
+}
+
+int apo_shard_state(apo_shard* r, double** pos_host, double** fit_host, int64_t* iterations_host) {
+    APO_CHECK(r, "shard is NULL");
+    if (pos_host) *pos_host = r->pos[r->cur];
+    if (fit_host) *fit_host = r->fit[r->cur];
+    if (iterations_host) *iterations_host = r->iters;
+    return APO_OK;
+}
+
+int apo_shard_counters(apo_shard* r, unsigned long long* trace_keys_host, int64_t n, int64_t* warnings_host) {
+    APO_CHECK(r && n >= 0 && n <= r->T, "bad arguments");
+    if (trace_keys_host)
+        APO_CUDA(cudaMemcpyAsync(trace_keys_host, r->trace_keys, 8 * ((size_t)n + 1), cudaMemcpyDeviceToHost,
+                                 r->stream));
+    unsigned long long w = 0;
+    APO_CUDA(cudaMemcpyAsync(&w, r->warn, 8, cudaMemcpyDeviceToHost, r->stream));
+    APO_CUDA(cudaStreamSynchronize(r->stream));
+    if (warnings_host) *warnings_host = (int64_t)w;
+    return APO_OK;
+}
+
+int apo_shard_destroy(apo_shard* r) {
+    if (!r) return APO_OK;
+    void* bufs[] = {r->order, r->keys_in, r->keys_out, r->vals_in, r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp,
+                    r->p_dr, r->cand_ok, r->trace_keys, r->warn};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete r;

@@ -41,6 +41,7 @@ struct UpdArgs {
     unsigned long long* trace_key;
     int cec_bufs;      // CEC2022 scratch rows (cec_bufs_for(code))
     uint8_t* cand_ok;  // non-null: candidates only (k_cec_eval finishes the update)
+    int rank_lo, rank_hi;  // 0-based rank range to update (rank_lo % 32 == 0); [0, ps) unless sharded
 };
 
 __device__ __forceinline__ void block_finish(unsigned long long my_min, unsigned my_warn,
@@ -130,15 +131,20 @@ __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group
     }
     unsigned long long my_min = ~0ull;
     unsigned my_warn = 0;
-    const int ngroups = (P.ps + 31) >> 5;
-    for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
+    const int g_hi = (A.rank_hi + 31) >> 5;
+    for (int grp = (A.rank_lo >> 5) + blockIdx.x * nwarps + warp; grp < g_hi; grp += gridDim.x * nwarps) {
         const int i0 = grp * 32 + 1;
-        const int n = min(32, P.ps - grp * 32);
+        const int n = min(32, A.rank_hi - grp * 32);
         if constexpr (SEL) {
             const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
             update_group<MAXC, OUT_SEL>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
                                         true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn, &ring_phase,
                                         A.cand_ok);
+        } else if (A.order) {  // sharded: rows addressed through the rank->row order, outputs by rank
+            const OrderedSlots R{A.pos, A.fit, A.order, P.ld};
+            update_group<MAXC, OUT_FIXUP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
+                                          A.out_fit, false, A.out_acc, A.out_warn, nullptr, g, lane, my_min,
+                                          my_warn, nullptr, A.cand_ok);
         } else {
             const DenseSlots R{A.pos, A.fit, P.ld};
             update_group<MAXC, OUT_FIXUP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
@@ -399,6 +405,8 @@ constexpr int kCecEvalMaxDim = 104;  // 13 register-resident n-tiles
 __host__ __device__ inline int cec_nt(int n) { return n <= 16 ? 2 : n <= 32 ? 4 : n <= 56 ? 7 : 13; }
 struct CecEvalArgs {
     int n_rows, dim, ld, bufs;
+    int row0;          // first row (dense: rank) of the range
+    const int* order;  // dense + sharded: old row/fitness of rank r at order[r] (nullable)
     ObjDesc O;
     const double* pos0;  // SEL
     const double* pos1;
@@ -433,8 +441,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_cec_eval(CecEvalArgs A) {
     unsigned my_warn = 0;
     const int ntiles = (A.n_rows + kCecRows - 1) / kCecRows;
     for (int tile = blockIdx.x * nwarps + warp; tile < ntiles; tile += gridDim.x * nwarps) {
-        const int r0 = tile * kCecRows;
-        const int nb = min(kCecRows, A.n_rows - r0);
+        const int r0 = A.row0 + tile * kCecRows;
+        const int nb = min(kCecRows, A.row0 + A.n_rows - r0);
         const int r = r0 + q;
         const bool live = q < nb;
         uint8_t cur = 0;
@@ -453,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_cec_eval(CecEvalArgs A) {
         const double nf = cec_eval_quad<NT>(A.O.cec, X, W, cs, dim, lane, ew);
         bool acc = false;
         if (live && t == 0) {
-            const double fit_i = A.fit[r];
+            const double fit_i = A.fit[(!SEL && A.order) ? A.order[r] : r];
             double kept = fit_i;
             bool warned = false;
             if (ok && isfinite(nf)) {
@@ -478,7 +486,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_cec_eval(CecEvalArgs A) {
             while (rej) {
                 const int qq = (__ffs(rej) - 1) >> 2;
                 rej &= rej - 1;
-                const double* x = A.pos + (size_t)(r0 + qq) * A.ld;
+                const int old_row = A.order ? A.order[r0 + qq] : r0 + qq;
+                const double* x = A.pos + (size_t)old_row * A.ld;
                 double* dst = A.out_pos + (size_t)(r0 + qq) * A.ld;
                 for (int d = lane; d < dim; d += 32) dst[d] = x[d];
             }
