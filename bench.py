@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-suite", action="store_true")
+    ap.add_argument("--no-shard", action="store_true")
     return ap.parse_args()
 
 
@@ -309,6 +310,11 @@ def bench_ours(args, rank, world, local):
         result["c4_" + other.split("_")[1]] = {
             "value": world * ps * K / (m2["max_ms"] / 1e3), "unit": UNIT, "ms_per_step": m2["max_ms"] / K,
             "workload": c4_workload(other, ps, dim), "roofline_kernels": m2["kernels"]}
+    if world > 1 and not args.no_shard:
+        try:
+            result["c4_sharded"] = bench_sharded(args, rank, world, local, K, W)
+        except Exception as exc:  # never lose the main line over the secondary measurement
+            result["c4_sharded"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if not args.no_e2e:
         result["e2e"] = bench_e2e(m["cfg"], m["obj"], K, rank, world)
     if not args.no_suite and rank == 0:
@@ -317,6 +323,37 @@ def bench_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(m["cfg"], args.objective)
     return result
+
+
+def bench_sharded(args, rank, world, local, K, W):
+    """C4 as BASELINE config 4 states it: ONE population of ps rows sharded by rank over the N GPUs,
+    per-iteration NCCL all-gather of the updated rows (strong scaling; shard.ShardedRun)."""
+    import torch
+
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200.shard import ShardedRun
+
+    ps, dim = args.ps, args.dim
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=max(100, K + W), seed=0)
+    run = ShardedRun(cfg, args.objective)
+    run.initialize()
+    run.iterate(W)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run.iterate(K)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    trace, _ = run.trace_and_warnings()
+    run.close()
+    return {"value": ps * K / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / K, "scaling": "strong",
+            "workload": f"C4 sharded: ONE population ps={ps} D={dim} {args.objective} split by rank over {world} GPUs, "
+                        "NCCL all-gather of rows + fitness per iteration",
+            "exchange_bytes_per_gpu_per_step": 8 * (dim + (dim & 1) + 1) * ps * (world - 1) / world,
+            "best": float(trace[-1])}
 
 
 def bench_e2e(cfg, obj, K, rank, world):

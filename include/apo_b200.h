@@ -74,7 +74,9 @@ typedef struct apo_objective {
     /* CEC2022, optional: rot_t zero-padded to [ncomp][round_up(dim,4)][8*nt]
      * with nt = dim<=16 ? 2 : dim<=32 ? 4 : dim<=56 ? 7 : 13 (dim <= 104).
      * When present, large populations evaluate in the DMMA kernel
-     * k_cec_eval; table may then hold the ELLIPS weights 10^(6i/(dim-1)). */
+     * k_cec_eval; table may then hold the ELLIPS weights 10^(6i/(dim-1)).
+     * For the hybrids (F6-F8) its output columns are permuted by the
+     * shuffle: rot_pad[0][i][j] = rot_t[0][i][shuffle[j]-1]. */
     const double *rot_pad;
 } apo_objective;
 

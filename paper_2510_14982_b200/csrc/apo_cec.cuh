@@ -545,23 +545,25 @@ __device__ __forceinline__ double qprod(double v) {
 // B through L1 from rot_pad.
 template <int NT>
 __device__ __forceinline__ void cec_rotate_quad(const double* __restrict__ rot_pad, double* Y, int ys, int n,
-                                                double off, int lane) {
+                                                double off, int lane, int bs = 8 * NT) {
+    // B: rot_pad in global memory (row stride 8 NT, read through L1) or a shared-memory copy with
+    // row stride bs = 8 NT + 4 (conflict-free: bs % 16 is 4 or 12)
     const int g = lane >> 2, t = lane & 3;
     const int n4 = (n + 3) & ~3;
     double acc[NT][2];
 #pragma unroll
     for (int k = 0; k < NT; k++) acc[k][0] = acc[k][1] = 0.0;
     double* yrow = Y + (size_t)g * ys;
-    const double* bp = rot_pad + (size_t)t * (8 * NT) + g;
+    const double* bp = rot_pad + (size_t)t * bs + g;
 #pragma unroll 2
     for (int i0 = 0; i0 < n4; i0 += 4) {
         const double a = yrow[i0 + t];
         double b[NT];
 #pragma unroll
-        for (int k = 0; k < NT; k++) b[k] = __ldg(bp + 8 * k);
+        for (int k = 0; k < NT; k++) b[k] = bp[8 * k];
 #pragma unroll
         for (int k = 0; k < NT; k++) dmma_m8n8k4(acc[k][0], acc[k][1], a, b[k]);
-        bp += 4 * (8 * NT);
+        bp += 4 * bs;
     }
     __syncwarp();
 #pragma unroll
@@ -692,7 +694,10 @@ __device__ inline double cec_basic_quad(int b, const double* z, int n, int t, co
 // compositions.  Every lane of quad q returns candidate q's fitness.
 template <int NT>
 __device__ inline double cec_eval_quad(const CecData& C, double* X, double* W, int xs, int n, int lane,
-                                       const double* ew) {
+                                       const double* ew, const double* bsm = nullptr) {
+    // bsm: shared-memory copy of rotation 0 (row stride 8 NT + 4), else rot_pad through L1
+    const double* B0 = bsm ? bsm : C.rot_pad;
+    const int bs0 = bsm ? 8 * NT + 4 : 8 * NT;
     const CecSpec& S = kCecSpec[C.fn - 1];
     const int q = lane >> 2, t = lane & 3;
     const int n4 = (n + 3) & ~3;
@@ -709,12 +714,14 @@ __device__ inline double cec_eval_quad(const CecData& C, double* X, double* W, i
             x[i] = (xi - oi) * sc;
         }
         __syncwarp();
-        cec_rotate_quad<NT>(C.rot_pad, X, xs, n, cec_offset(b), lane);
+        cec_rotate_quad<NT>(B0, X, xs, n, cec_offset(b), lane, bs0);
         f = cec_basic_quad(b, x, n, t, ew);
     } else if (S.kind == 1) {
+        // rot_pad's output columns are pre-permuted by the shuffle (objectives.py), so the rotation
+        // leaves z[shuffle[j]-1] in column j: the segments are contiguous, no gather
         for (int i = t; i < n; i += 4) x[i] = x[i] - C.shift[i];
         __syncwarp();
-        cec_rotate_quad<NT>(C.rot_pad, X, xs, n, 0.0, lane);
+        cec_rotate_quad<NT>(B0, X, xs, n, 0.0, lane, bs0);
         int sizes[6];
         int tot = 0;
         for (int k = 0; k < S.ncomp - 1; k++) {
@@ -726,13 +733,14 @@ __device__ inline double cec_eval_quad(const CecData& C, double* X, double* W, i
         int start = 0;
         for (int k = 0; k < S.ncomp; k++) {
             const double sc = cec_scale(S.basic[k]), off = cec_offset(S.basic[k]);
-            for (int i = t; i < sizes[k]; i += 4) w[start + i] = x[C.shuffle[start + i] - 1] * sc + off;
-            start += sizes[k];
+            const int end = start + sizes[k];
+            for (int i = start + ((t - start) & 3); i < end; i += 4) x[i] = x[i] * sc + off;
+            start = end;
         }
         __syncwarp();
         start = 0;
         for (int k = 0; k < S.ncomp; k++) {
-            if (sizes[k] > 0) f += cec_basic_quad(S.basic[k], w + start, sizes[k], t, ew);
+            if (sizes[k] > 0) f += cec_basic_quad(S.basic[k], x + start, sizes[k], t, ew);
             start += sizes[k];
         }
     } else {

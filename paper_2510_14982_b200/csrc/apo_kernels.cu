@@ -292,7 +292,7 @@ __global__ void k_debug_exp(const double* x, double* out, long long n) {
 // k_cec_eval evaluates them in DMMA tiles and finishes the update.
 // mid_event (nullable) is recorded between the two.
 int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* cand_ok = nullptr,
-                  cudaEvent_t mid_event = nullptr) {
+                  cudaEvent_t mid_event = nullptr, unsigned* tile_counter = nullptr) {
     UpdArgs a = A0;
     const int dim = a.P.dim;
     const bool group = dim <= kGroupMaxDim;
@@ -329,7 +329,7 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     E.ld = a.P.ld;
     E.O = a.O;
     const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
-    E.bufs = (fn_id >= 6) ? 2 : 1;
+    E.bufs = (fn_id >= 9) ? 1 : 0;  // compositions keep the candidate and need W (hybrids permute in rot_pad)
     E.pos0 = a.pos0;
     E.pos1 = a.pos1;
     E.sel = a.sel;
@@ -343,17 +343,37 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     E.cand_ok = cand_ok;
     E.warn_count = a.warn_count;
     E.trace_key = a.trace_key;
-    const void* fe = pick_cec_eval(sel_mode, dim);
-    const size_t esmem = cec_eval_warp_bytes(dim, E.bufs) * kWarps;
+    // F1-F8 (one rotation): rotation staged in SMEM, X double-buffered, as many warps as fit (<= 16);
+    // compositions: B through L1, 8 warps, 2 CTAs/SM
+    const bool fast = fn_id <= 8;
+    const void* fe = pick_cec_eval(sel_mode, dim, fast);
+    int ewarps = kWarps;
+    size_t esmem = cec_eval_warp_bytes(dim, E.bufs, fast) * kWarps;
+    if (fast) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+            optin = 227 * 1024;
+        const size_t bsm = cec_bsm_bytes(dim, cec_nt(dim));
+        const size_t per = cec_eval_warp_bytes(dim, E.bufs, true);
+        ewarps = (int)(((size_t)optin - bsm) / per);
+        if (ewarps > 16) ewarps = 16;
+        if (ewarps >= 4) ewarps &= ~3;  // equal warps per SM sub-partition (they share its DMMA pipe)
+        APO_CHECK(ewarps >= 1, "k_cec_eval: dim too large for the shared-memory rotation");
+        esmem = bsm + per * (size_t)ewarps;
+    }
     if (int rc = set_smem(fe, esmem)) return rc;
     int eper = 1;
-    APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&eper, fe, kThreads, esmem));
+    APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&eper, fe, 32 * ewarps, esmem));
     if (eper < 1) eper = 1;
     const long long tiles = ((long long)E.n_rows + kCecRows - 1) / kCecRows;
-    const long long eneed = (tiles + kWarps - 1) / kWarps;
+    const long long eneed = (tiles + ewarps - 1) / ewarps;
     const long long ecap = (long long)eper * num_sms();
+    APO_CHECK(tile_counter != nullptr, "k_cec_eval needs a tile counter");
+    E.tile_counter = tile_counter;
+    APO_CUDA(cudaMemsetAsync(tile_counter, 0, sizeof(unsigned), st));
     void* eargs[] = {(void*)&E};
-    APO_CUDA(cudaLaunchKernel(fe, dim3((unsigned)(eneed < ecap ? eneed : ecap)), dim3(kThreads), eargs, esmem, st));
+    APO_CUDA(cudaLaunchKernel(fe, dim3((unsigned)(eneed < ecap ? eneed : ecap)), dim3(32 * ewarps), eargs, esmem, st));
     return APO_OK;
 }
 
@@ -431,6 +451,7 @@ struct apo_run {
     size_t tmp_bytes;
     double* p_dr;
     uint8_t* cand_ok;  // CEC2022 split update: per-slot candidate finiteness
+    unsigned* tile_counter;
     std::vector<double> sched;
     unsigned long long* trace_keys;  // [T+1]
     unsigned long long* warn;
@@ -495,8 +516,10 @@ int apo_run_updates_obj(const double* positions, const double* fitness, const ui
     A.cec_bufs = cec_bufs_for(A.O.code);
     uint8_t* cand_ok = nullptr;
     const bool cec = A.O.code > APO_OBJ_CEC2022_BASE;
-    if (cec) APO_CUDA(cudaMallocAsync((void**)&cand_ok, (size_t)ps, as_stream(stream)));
-    const int rc = launch_update(false, A, as_stream(stream), cand_ok);
+    const size_t ok_bytes = ((size_t)ps + 15) & ~(size_t)15;  // cand_ok, then the k_cec_eval tile counter
+    if (cec) APO_CUDA(cudaMallocAsync((void**)&cand_ok, ok_bytes + 16, as_stream(stream)));
+    unsigned* counter = cec ? reinterpret_cast<unsigned*>(cand_ok + ok_bytes) : nullptr;
+    const int rc = launch_update(false, A, as_stream(stream), cand_ok, nullptr, counter);
     if (cec) cudaFreeAsync(cand_ok, as_stream(stream));
     return rc;
 }
@@ -693,6 +716,7 @@ int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iteration
     alloc(&r->tmp, r->tmp_bytes);
     alloc((void**)&r->p_dr, 8 * (size_t)ps);
     alloc((void**)&r->cand_ok, (size_t)ps);
+    alloc((void**)&r->tile_counter, 16);
     alloc((void**)&r->trace_keys, 8 * (size_t)(max_iterations + 1));
     alloc((void**)&r->warn, 8);
     if (e != cudaSuccess) {
@@ -789,7 +813,7 @@ int apo_run_iterate(apo_run* r, int64_t n) {
         A.warn_count = r->warn;
         A.trace_key = r->trace_keys + t + 1;
         A.cec_bufs = cec_bufs_for(r->obj.code);
-        if (int rc = launch_update(true, A, st, r->cand_ok, ev[1])) return rc;
+        if (int rc = launch_update(true, A, st, r->cand_ok, ev[1], r->tile_counter)) return rc;
         if (r->profile) APO_CUDA(cudaEventRecord(ev[2], st));
         r->cur ^= 1;
         r->iters++;
@@ -907,7 +931,8 @@ int apo_run_destroy(apo_run* r) {
     if (!r) return APO_OK;
     clear_profile(r);
     void* bufs[] = {r->pos[0], r->pos[1], r->sel[0], r->sel[1], r->fit[0], r->fit[1], r->order, r->keys_in, r->keys_out, r->vals_in,
-                    r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn, r->cand_ok};
+                    r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn, r->cand_ok,
+                    r->tile_counter};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete r;
@@ -942,6 +967,7 @@ struct apo_shard {
     size_t tmp_bytes;
     double* p_dr;
     uint8_t* cand_ok;
+    unsigned* tile_counter;
     unsigned long long* trace_keys;  // [T+1], this process's ranks only (reduce MIN across processes)
     unsigned long long* warn;        // this process's ranks only (reduce SUM)
     std::vector<double> sched;
@@ -1000,6 +1026,7 @@ int apo_shard_create(apo_shard** out, int64_t ps, int64_t dim, int64_t ld, int64
     alloc(&r->tmp, r->tmp_bytes);
     alloc((void**)&r->p_dr, 8 * (size_t)ps);
     alloc((void**)&r->cand_ok, (size_t)ps);
+    alloc((void**)&r->tile_counter, 16);
     alloc((void**)&r->trace_keys, 8 * (size_t)(max_iterations + 1));
     alloc((void**)&r->warn, 8);
     if (e != cudaSuccess) {
@@ -1083,7 +1110,7 @@ int apo_shard_update_range(apo_shard* r, int64_t lo, int64_t hi) {
     A.cec_bufs = cec_bufs_for(r->obj.code);
     A.rank_lo = (int)lo;
     A.rank_hi = (int)hi;
-    return launch_update(false, A, r->stream, r->cand_ok);
+    return launch_update(false, A, r->stream, r->cand_ok, nullptr, r->tile_counter);
 }
 
 int apo_shard_end(apo_shard* r) {
@@ -1116,7 +1143,7 @@ int apo_shard_counters(apo_shard* r, unsigned long long* trace_keys_host, int64_
 int apo_shard_destroy(apo_shard* r) {
     if (!r) return APO_OK;
     void* bufs[] = {r->order, r->keys_in, r->keys_out, r->vals_in, r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp,
-                    r->p_dr, r->cand_ok, r->trace_keys, r->warn};
+                    r->p_dr, r->cand_ok, r->tile_counter, r->trace_keys, r->warn};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete r;

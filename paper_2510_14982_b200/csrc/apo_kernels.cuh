@@ -421,47 +421,128 @@ struct CecEvalArgs {
     const uint8_t* cand_ok;
     unsigned long long* warn_count;
     unsigned long long* trace_key;
+    unsigned* tile_counter;  // zeroed before the launch: warps claim 8-row tiles dynamically
 };
 
-__host__ __device__ inline size_t cec_eval_warp_bytes(int dim, int bufs) {
-    return 8 * (size_t)bufs * kCecRows * (size_t)cec_stride(dim);
+// FAST (F1-F8: one rotation): the CTA stages that rotation in shared memory
+// once (persistent CTAs) and every warp double-buffers its X tile with
+// cp.async, so the next tile's candidate rows stream in while this one is
+// evaluated.  Otherwise (compositions: up to 6 rotations) B is read through
+// L1 and each warp has one X tile plus W.
+__host__ __device__ inline int cec_bsm_stride(int nt) { return 8 * nt + 4; }
+__host__ __device__ inline size_t cec_eval_warp_bytes(int dim, int bufs, bool fast) {
+    return 8 * (size_t)((fast ? 2 : 1) + bufs) * kCecRows * (size_t)cec_stride(dim);  // bufs = W buffers
+}
+__host__ __device__ inline size_t cec_bsm_bytes(int dim, int nt) {  // rotation + shift vector
+    return 8 * (size_t)((dim + 3) & ~3) * (size_t)cec_bsm_stride(nt) + 8 * (size_t)((dim + 1) & ~1);
 }
 
-template <bool SEL, int NT>
-__global__ void __launch_bounds__(kThreads, 2) k_cec_eval(CecEvalArgs A) {
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <bool SEL, int NT, bool FAST>
+__global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int q = lane >> 2, t = lane & 3;  // quad q owns row q of the tile
     const int dim = A.dim, cs = cec_stride(dim), n4 = (dim + 3) & ~3;
-    double* X = reinterpret_cast<double*>(smem + (size_t)warp * cec_eval_warp_bytes(dim, A.bufs));
-    double* W = X + (size_t)kCecRows * cs;
-    double* xrow = X + (size_t)q * cs;
+    double* base = reinterpret_cast<double*>(smem + (size_t)warp * cec_eval_warp_bytes(dim, A.bufs, FAST));
+    double* Xb[2] = {base, base + (size_t)kCecRows * cs};
+    double* W = base + (size_t)(FAST ? 2 : 1) * kCecRows * cs;  // compositions only
+    double* bsm = nullptr;
+    CecData C = A.O.cec;
+    if constexpr (FAST) {
+        bsm = reinterpret_cast<double*>(smem + (size_t)nwarps * cec_eval_warp_bytes(dim, A.bufs, true));
+        const int bs = cec_bsm_stride(NT), w8 = 8 * NT;
+        for (int e = threadIdx.x; e < n4 * w8; e += blockDim.x) {
+            const int i = e / w8, j = e - i * w8;
+            bsm[i * bs + j] = C.rot_pad[e];
+        }
+        double* osm = bsm + (size_t)n4 * bs;  // the shift vector too (read once per element per tile)
+        for (int i = threadIdx.x; i < dim; i += blockDim.x) osm[i] = C.shift[i];
+        C.shift = osm;
+        __syncthreads();
+    }
     const double* ew = A.O.table_len >= dim ? A.O.table : nullptr;  // ELLIPS weights (host libm)
     unsigned long long my_min = ~0ull;
     unsigned my_warn = 0;
     const int ntiles = (A.n_rows + kCecRows - 1) / kCecRows;
-    for (int tile = blockIdx.x * nwarps + warp; tile < ntiles; tile += gridDim.x * nwarps) {
+    const int stride = gridDim.x * nwarps;
+    auto row_of = [&](int tile) { return A.row0 + tile * kCecRows + q; };
+    auto live_in = [&](int tile) { return tile < ntiles && row_of(tile) < A.row0 + A.n_rows; };
+    // row q of `tile` -> X tile `buf` (cp.async); pads and dead rows are zero
+    auto issue = [&](int tile, int buf, uint8_t selq) {
+        double* xrow = Xb[buf] + (size_t)q * cs;
+        const bool live = live_in(tile);
+        const double* src = nullptr;
+        if (live) {
+            const int r = row_of(tile);
+            if constexpr (SEL) src = (selq ? A.pos0 : A.pos1) + (size_t)r * A.ld;  // the slot's alternate buffer
+            else src = A.out_pos + (size_t)r * A.ld;
+        }
+        for (int i = t; i < n4; i += 4) {
+            if (live && i < dim) cp_async8(xrow + i, src + i);
+            else xrow[i] = 0.0;
+        }
+    };
+    auto sel_of = [&](int tile) -> uint8_t {
+        if constexpr (SEL) return live_in(tile) ? A.sel[row_of(tile)] : (uint8_t)0;
+        return 0;
+    };
+    // dynamic tile claims (lane 0 + broadcast) keep the warps of an SM finishing together
+    auto claim = [&]() -> int {
+        unsigned v = 0;
+        if (lane == 0) v = atomicAdd(A.tile_counter, 1u);
+        return (int)__shfl_sync(kFull, v, 0);
+    };
+    (void)stride;
+    int tile = claim();
+    int tile_nxt = 0;
+    uint8_t sel_cur = sel_of(tile), sel_nxt = 0;
+    if constexpr (FAST) {
+        if (tile < ntiles) issue(tile, 0, sel_cur);
+        cp_async_commit();
+        tile_nxt = claim();
+        sel_nxt = sel_of(tile_nxt);
+    }
+    int buf = 0;
+    while (tile < ntiles) {
         const int r0 = A.row0 + tile * kCecRows;
         const int nb = min(kCecRows, A.row0 + A.n_rows - r0);
         const int r = r0 + q;
         const bool live = q < nb;
-        uint8_t cur = 0;
-        const double* src = nullptr;
-        if (live) {
-            if constexpr (SEL) {
-                cur = A.sel[r];
-                src = (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld;  // the slot's alternate buffer
-            } else {
-                src = A.out_pos + (size_t)r * A.ld;
-            }
+        // per-row scalars for the select, loaded early so their latency hides behind the evaluation
+        bool ok = false;
+        double fit_i = 0.0;
+        if (live && t == 0) {
+            ok = A.cand_ok[r] != 0;
+            fit_i = A.fit[(!SEL && A.order) ? A.order[r] : r];
         }
-        for (int i = t; i < n4; i += 4) xrow[i] = (live && i < dim) ? src[i] : 0.0;
-        const bool ok = live && A.cand_ok[r] != 0;
+        const uint8_t cur = sel_cur;
+        int tile_next;
+        if constexpr (FAST) {
+            tile_next = tile_nxt;
+            if (tile_next < ntiles) issue(tile_next, buf ^ 1, sel_nxt);
+            cp_async_commit();
+            sel_cur = sel_nxt;
+            tile_nxt = tile_next < ntiles ? claim() : ntiles;
+            sel_nxt = sel_of(tile_nxt);
+            cp_async_wait_prev();
+        } else {
+            issue(tile, 0, cur);
+            cp_async_commit();
+            tile_next = claim();
+            sel_cur = sel_of(tile_next);
+            cp_async_wait_all();
+        }
         __syncwarp();
-        const double nf = cec_eval_quad<NT>(A.O.cec, X, W, cs, dim, lane, ew);
+        const double nf = cec_eval_quad<NT>(C, Xb[buf], W, cs, dim, lane, ew, bsm);
         bool acc = false;
         if (live && t == 0) {
-            const double fit_i = A.fit[(!SEL && A.order) ? A.order[r] : r];
             double kept = fit_i;
             bool warned = false;
             if (ok && isfinite(nf)) {
@@ -493,7 +574,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_cec_eval(CecEvalArgs A) {
             }
         }
         __syncwarp();
+        if constexpr (FAST) buf ^= 1;
+        tile = tile_next;
     }
+    cp_async_wait_all();
     block_finish(my_min, my_warn, A.warn_count, A.trace_key);
 }
 
@@ -501,6 +585,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_cec_eval(CecEvalArgs A) {
 const void* pick_update_sel(int dim);
 const void* pick_update_dense(int dim);
 const void* pick_run_batch(int dim);
-const void* pick_cec_eval(bool sel, int dim);
+const void* pick_cec_eval(bool sel, int dim, bool fast);
 
 }  // namespace apo

@@ -177,6 +177,8 @@ class DeviceObjective:
                 n4 = (dim + 3) // 4 * 4
                 pad = np.zeros((rot_t.shape[0], n4, 8 * nt))
                 pad[:, :dim, :dim] = rot_t
+                if obj.code - 100 in (6, 7, 8):  # hybrids: output column j holds z[shuffle[j]-1]
+                    pad[0, :dim, :dim] = rot_t[0][:, np.asarray(shuffle) - 1]
                 arrays.append(("rot_pad", pad))
                 table = elliptic_weights(dim)  # ELLIPS weights 10^(6i/(D-1)), host libm like the oracle
             for field, arr in arrays:

@@ -79,5 +79,11 @@ int main() {
     const double lat = msl * 1e-3 * clk * 1e3 / iters;
     printf("{\"dfma_tflops\": %.2f, \"dmma_tflops_1chain\": %.2f, \"dmma_tflops_4chain\": %.2f, "
            "\"dmma_latency_cycles\": %.1f, \"sms\": %d}\n", dfma, dmma1, dmma4, lat, sms);
+    // DMMA throughput vs warps per SM (one CTA of W warps per SM, 13 independent accumulators per warp)
+    for (int w : {4, 8, 12, 16, 32}) {
+        float m = time_it([&] { k_dmma<13><<<sms, 32 * w>>>(out, iters / 4, 1.0000001, 1e-7); });
+        printf("{\"warps_per_sm\": %d, \"chains\": 13, \"dmma_tflops\": %.2f}\n", w,
+               2.0 * 256 * 13 * (iters / 4) * (double)w * sms / (m * 1e-3) / 1e12);
+    }
     return 0;
 }
