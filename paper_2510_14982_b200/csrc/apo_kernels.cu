@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -348,19 +349,26 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     const bool fast = fn_id <= 8;
     const void* fe = pick_cec_eval(sel_mode, dim, fast);
     int ewarps = kWarps;
-    size_t esmem = cec_eval_warp_bytes(dim, E.bufs, fast) * kWarps;
+    E.prefetch = 0;
+    size_t esmem = cec_eval_warp_bytes(dim, E.bufs, false) * kWarps;
     if (fast) {
         int dev = 0, optin = 0;
         cudaGetDevice(&dev);
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
             optin = 227 * 1024;
+        static const int env_pf = getenv("APO_CEC_PREFETCH") ? atoi(getenv("APO_CEC_PREFETCH")) : -1;
         const size_t bsm = cec_bsm_bytes(dim, cec_nt(dim));
-        const size_t per = cec_eval_warp_bytes(dim, E.bufs, true);
-        ewarps = (int)(((size_t)optin - bsm) / per);
-        if (ewarps > 16) ewarps = 16;
-        if (ewarps >= 4) ewarps &= ~3;  // equal warps per SM sub-partition (they share its DMMA pipe)
+        auto fit_warps = [&](bool pf) {
+            int w = (int)(((size_t)optin - bsm) / cec_eval_warp_bytes(dim, E.bufs, pf));
+            if (w > 16) w = 16;
+            if (w >= 4) w &= ~3;  // equal warps per SM sub-partition (they share its DMMA pipe)
+            return w;
+        };
+        // prefetch (double-buffered X) unless dropping it buys more warps per SM
+        E.prefetch = env_pf >= 0 ? env_pf : (fit_warps(false) > fit_warps(true) ? 0 : 1);
+        ewarps = fit_warps(E.prefetch != 0);
         APO_CHECK(ewarps >= 1, "k_cec_eval: dim too large for the shared-memory rotation");
-        esmem = bsm + per * (size_t)ewarps;
+        esmem = bsm + cec_eval_warp_bytes(dim, E.bufs, E.prefetch != 0) * (size_t)ewarps;
     }
     if (int rc = set_smem(fe, esmem)) return rc;
     int eper = 1;

@@ -422,6 +422,7 @@ struct CecEvalArgs {
     unsigned long long* warn_count;
     unsigned long long* trace_key;
     unsigned* tile_counter;  // zeroed before the launch: warps claim 8-row tiles dynamically
+    int prefetch;            // FAST: double-buffer X with cp.async (else one X tile per warp, more warps)
 };
 
 // FAST (F1-F8: one rotation): the CTA stages that rotation in shared memory
@@ -430,8 +431,8 @@ struct CecEvalArgs {
 // evaluated.  Otherwise (compositions: up to 6 rotations) B is read through
 // L1 and each warp has one X tile plus W.
 __host__ __device__ inline int cec_bsm_stride(int nt) { return 8 * nt + 4; }
-__host__ __device__ inline size_t cec_eval_warp_bytes(int dim, int bufs, bool fast) {
-    return 8 * (size_t)((fast ? 2 : 1) + bufs) * kCecRows * (size_t)cec_stride(dim);  // bufs = W buffers
+__host__ __device__ inline size_t cec_eval_warp_bytes(int dim, int bufs, bool prefetch) {
+    return 8 * (size_t)((prefetch ? 2 : 1) + bufs) * kCecRows * (size_t)cec_stride(dim);  // bufs = W buffers
 }
 __host__ __device__ inline size_t cec_bsm_bytes(int dim, int nt) {  // rotation + shift vector
     return 8 * (size_t)((dim + 3) & ~3) * (size_t)cec_bsm_stride(nt) + 8 * (size_t)((dim + 1) & ~1);
@@ -450,13 +451,14 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int q = lane >> 2, t = lane & 3;  // quad q owns row q of the tile
     const int dim = A.dim, cs = cec_stride(dim), n4 = (dim + 3) & ~3;
-    double* base = reinterpret_cast<double*>(smem + (size_t)warp * cec_eval_warp_bytes(dim, A.bufs, FAST));
+    const bool pf = FAST && A.prefetch;
+    double* base = reinterpret_cast<double*>(smem + (size_t)warp * cec_eval_warp_bytes(dim, A.bufs, pf));
     double* Xb[2] = {base, base + (size_t)kCecRows * cs};
-    double* W = base + (size_t)(FAST ? 2 : 1) * kCecRows * cs;  // compositions only
+    double* W = base + (size_t)(pf ? 2 : 1) * kCecRows * cs;  // compositions only
     double* bsm = nullptr;
     CecData C = A.O.cec;
     if constexpr (FAST) {
-        bsm = reinterpret_cast<double*>(smem + (size_t)nwarps * cec_eval_warp_bytes(dim, A.bufs, true));
+        bsm = reinterpret_cast<double*>(smem + (size_t)nwarps * cec_eval_warp_bytes(dim, A.bufs, pf));
         const int bs = cec_bsm_stride(NT), w8 = 8 * NT;
         for (int e = threadIdx.x; e < n4 * w8; e += blockDim.x) {
             const int i = e / w8, j = e - i * w8;
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     int tile = claim();
     int tile_nxt = 0;
     uint8_t sel_cur = sel_of(tile), sel_nxt = 0;
-    if constexpr (FAST) {
+    if (pf) {
         if (tile < ntiles) issue(tile, 0, sel_cur);
         cp_async_commit();
         tile_nxt = claim();
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         }
         const uint8_t cur = sel_cur;
         int tile_next;
-        if constexpr (FAST) {
+        if (pf) {
             tile_next = tile_nxt;
             if (tile_next < ntiles) issue(tile_next, buf ^ 1, sel_nxt);
             cp_async_commit();
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
             }
         }
         __syncwarp();
-        if constexpr (FAST) buf ^= 1;
+        if (pf) buf ^= 1;
         tile = tile_next;
     }
     cp_async_wait_all();
