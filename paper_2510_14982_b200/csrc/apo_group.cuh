@@ -489,7 +489,10 @@ enum OutMode : int {
 // Candidate of member p (rank i) of the group, warp-cooperative: computes
 // the clamped candidate, writes it to `cand_out`, stores its fitness terms in
 // rows (T1, T2) and returns the finiteness vote.
-template <int MAXC, bool MANY, class Rows>
+// Objective classes an update kernel is compiled for (keeps CEC code out of kernels that never see it).
+enum GroupKind : int { KIND_ANY = 0, KIND_BASIC = 1, KIND_CAND = 2 };
+
+template <int MAXC, bool MANY, bool CO, class Rows>
 __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, const Rows& R, int i, int p,
                                        double* cand_out, double* T1, double* T2, const GroupScratch& g, int lane,
                                        const double* staged) {
@@ -531,15 +534,20 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
         return xd + (f * direction) * mk(d);
     };
     // every lane calls finish() once per chunk (the shuffles need the full warp)
+    // CO (candidates only, CEC2022 on HBM): no fitness terms; only rosenbrock needs the d-1 neighbour
+    const bool need_prev = !CO && O.code == OBJ_ROSENBROCK;
     auto finish = [&](int d, double c, bool valid) {
         c = clampv(c, P.lower, P.upper);
-        double prev = __shfl_up_sync(kFull, c, 1);
-        if (lane == 0) prev = carry;
-        carry = __shfl_sync(kFull, c, 31);
+        double prev = 0.0;
+        if (need_prev) {
+            prev = __shfl_up_sync(kFull, c, 1);
+            if (lane == 0) prev = carry;
+            carry = __shfl_sync(kFull, c, 31);
+        }
         if (valid) {
             ok = ok && isfinite(c);
             cand_out[d] = c;
-            write_terms(O, T1, T2, d, c, prev);
+            if constexpr (!CO) write_terms(O, T1, T2, d, c, prev);
         }
     };
 
@@ -593,7 +601,7 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
 //                 out_fit (by slot) record the kept state.
 // MODE OUT_FIXUP: candidates go to out_rows (by slot if out_by_slot, else by
 //                 rank); rejected rows are then rewritten with the old row.
-template <int MAXC, int MODE, class Rows>
+template <int MAXC, int MODE, int KIND, class Rows>
 __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const Rows& R, int i0, int n,
                                     const uint8_t* in_dr_bytes, const unsigned* in_dr_bits, const double* p_dr,
                                     double* out_rows, double* out_fit, bool out_by_slot, uint8_t* out_acc,
@@ -630,11 +638,12 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
         for (int p = 0; p < kStages && p < n; p++) issue(p);
     }
     const bool two = two_term_arrays(O.code);
-    const bool cec = O.code >= OBJ_CEC_BASE;
+    // KIND_BASIC kernels are never launched for CEC2022 objectives (the host routes those elsewhere)
+    const bool cec = KIND == KIND_ANY && O.code >= OBJ_CEC_BASE;
     const int ts = cec ? g.cstride : g.tstride;
     // cand_ok != nullptr: candidates only (written + finiteness flag); the
     // fitness, greedy select and best-so-far run in k_cec_eval (CEC2022 on HBM).
-    const bool cand_only = cand_ok != nullptr;
+    constexpr bool cand_only = KIND == KIND_CAND;  // cand_ok must then be non-null
     const int B = cand_only ? 32 : cec ? kCecRows : two ? g.batch / 2 : g.batch;
     double* T2base = g.T + (size_t)(g.batch / 2) * g.tstride;
     for (int h = 0; h < n; h += B) {
@@ -656,8 +665,8 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
                 staged = g.ring + (size_t)st * 4 * g.rld;
             }
             const bool ok = P.npairs > 1
-                                ? group_candidate<MAXC, true>(P, O, R, i, p, dst, T1, T2, g, lane, staged)
-                                : group_candidate<MAXC, false>(P, O, R, i, p, dst, T1, T2, g, lane, staged);
+                                ? group_candidate<MAXC, true, cand_only>(P, O, R, i, p, dst, T1, T2, g, lane, staged)
+                                : group_candidate<MAXC, false, cand_only>(P, O, R, i, p, dst, T1, T2, g, lane, staged);
             okmask |= (ok ? 1u : 0u) << q;
             if (staging) {
                 __syncwarp();
@@ -665,7 +674,7 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
             }
         }
         __syncwarp();
-        if (cand_only) {
+        if constexpr (cand_only) {
             if (lane < nb) {
                 const int own_key = g.slot[4 * (h + lane)];
                 cand_ok[MODE == OUT_SEL ? R.slot_of(own_key) : i0 - 1 + h + lane] = (uint8_t)((okmask >> lane) & 1u);
@@ -675,9 +684,11 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
         }
         bool acc = false, warned = false;
         double cec_f = 0.0;
-        if (cec)  // the batch's staged candidates together (DMMA rotation, apo_cec.cuh)
-            cec_f = cec_eval_batch(O.cec, g.T, g.T + (size_t)kCecRows * ts, g.T + (size_t)2 * kCecRows * ts, ts, nb,
-                                   P.dim, lane);
+        if constexpr (KIND == KIND_ANY) {
+            if (cec)  // the batch's staged candidates together (DMMA rotation, apo_cec.cuh)
+                cec_f = cec_eval_batch(O.cec, g.T, g.T + (size_t)kCecRows * ts, g.T + (size_t)2 * kCecRows * ts, ts,
+                                       nb, P.dim, lane);
+        }
         if (lane < nb) {
             const int p = h + lane, i = i0 + p;
             const int own_key = g.slot[4 * p];
@@ -685,7 +696,7 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
             const double fit_i = R.fit_at(own);
             double kept = fit_i;
             if ((okmask >> lane) & 1u) {
-                const double nf = O.code >= OBJ_CEC_BASE
+                const double nf = cec
                                       ? cec_f
                                       : fold_terms(O, g.T + (size_t)lane * g.tstride,
                                                    two ? T2base + (size_t)lane * g.tstride : nullptr, P.dim);

@@ -306,7 +306,8 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     const int w = group ? kWarps : warps_for_dim(dim);
     const bool stage = sel_mode && dim <= APO_STAGE_MAX_DIM;
     const size_t smem = (group ? group_scratch_bytes(dim, stage, a.cec_bufs) : warp_scratch_bytes(dim)) * (size_t)w;
-    const void* fn = sel_mode ? pick_update_sel(dim) : pick_update_dense(dim);
+    const bool cec = a.O.code > APO_OBJ_CEC2022_BASE;
+    const void* fn = sel_mode ? pick_update_sel(dim, split, cec) : pick_update_dense(dim, split, cec);
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));

@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(kThreads) k_update(UpdArgs A) {
 #ifndef APO_GROUP_MIN_BLOCKS
 #define APO_GROUP_MIN_BLOCKS 2
 #endif
-template <bool SEL, int MAXC>
+// KIND: KIND_ANY (every objective), KIND_BASIC (no CEC2022 code), KIND_CAND
+// (candidates only: the CEC2022 split, k_cec_eval finishes the update).
+template <bool SEL, int MAXC, int KIND>
 __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group(UpdArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const IterParams& P = A.P;
@@ -137,17 +139,17 @@ __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group
         const int n = min(32, A.rank_hi - grp * 32);
         if constexpr (SEL) {
             const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
-            update_group<MAXC, OUT_SEL>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
+            update_group<MAXC, OUT_SEL, KIND>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
                                         true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn, &ring_phase,
                                         A.cand_ok);
         } else if (A.order) {  // sharded: rows addressed through the rank->row order, outputs by rank
             const OrderedSlots R{A.pos, A.fit, A.order, P.ld};
-            update_group<MAXC, OUT_FIXUP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
+            update_group<MAXC, OUT_FIXUP, KIND>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
                                           A.out_fit, false, A.out_acc, A.out_warn, nullptr, g, lane, my_min,
                                           my_warn, nullptr, A.cand_ok);
         } else {
             const DenseSlots R{A.pos, A.fit, P.ld};
-            update_group<MAXC, OUT_FIXUP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
+            update_group<MAXC, OUT_FIXUP, KIND>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
                                           A.out_fit, false, A.out_acc, A.out_warn, nullptr, g, lane, my_min,
                                           my_warn, nullptr, A.cand_ok);
         }
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
             const int G = min(32, (ps + nwarps - 1) / nwarps);
             for (int q = warp; q * G < ps; q += nwarps) {
                 const int i0 = q * G + 1;
-                update_group<MAXC, OUT_FIXUP>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr, pos[nxt],
+                update_group<MAXC, OUT_FIXUP, KIND_ANY>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr, pos[nxt],
                                               fit[nxt], true, nullptr, nullptr, nullptr, g, lane, my_min, my_warn);
             }
             __syncthreads();
@@ -584,8 +586,8 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
 }
 
 // Kernel getters (defined in the instantiating TUs).
-const void* pick_update_sel(int dim);
-const void* pick_update_dense(int dim);
+const void* pick_update_sel(int dim, bool cand_only, bool cec);
+const void* pick_update_dense(int dim, bool cand_only, bool cec);
 const void* pick_run_batch(int dim);
 const void* pick_cec_eval(bool sel, int dim, bool fast);
 

@@ -4,12 +4,22 @@
 
 namespace apo {
 
-const void* pick_update_dense(int dim) {
-    if (dim <= 32) return (const void*)k_update_group<false, 1>;
-    if (dim <= 64) return (const void*)k_update_group<false, 2>;
-    if (dim <= 128) return (const void*)k_update_group<false, 4>;
-    if (dim <= kGroupMaxDim) return (const void*)k_update_group<false, 0>;
-    return (const void*)k_update<false>;
+// cand_only: the CEC2022 split path (dim <= kCecEvalMaxDim).  Fused CEC2022
+// (no split available) always takes the generic MAXC = 0 kernel so the
+// register-resident variants carry no CEC code.
+const void* pick_update_dense(int dim, bool cand_only, bool cec) {
+    if (cand_only) {
+        if (dim <= 32) return (const void*)k_update_group<false, 1, KIND_CAND>;
+        if (dim <= 64) return (const void*)k_update_group<false, 2, KIND_CAND>;
+        if (dim <= 128) return (const void*)k_update_group<false, 4, KIND_CAND>;
+        return nullptr;
+    }
+    if (dim > kGroupMaxDim) return (const void*)k_update<false>;
+    if (cec) return (const void*)k_update_group<false, 0, KIND_ANY>;
+    if (dim <= 32) return (const void*)k_update_group<false, 1, KIND_BASIC>;
+    if (dim <= 64) return (const void*)k_update_group<false, 2, KIND_BASIC>;
+    if (dim <= 128) return (const void*)k_update_group<false, 4, KIND_BASIC>;
+    return (const void*)k_update_group<false, 0, KIND_ANY>;
 }
 
 }  // namespace apo
