@@ -107,18 +107,27 @@ __device__ __forceinline__ double grie_rosen_t(double a, double b) {
     const double t = 100.0 * t1 * t1 + t2 * t2;
     return t * t / 4000.0 - cos(t) + 1.0;
 }
+// fmod(a, 500) for a >= 0, exactly: k*500 is exact, a - k*500 is exact (Sterbenz), and the
+// only misstep of k = floor(a/500) is a quotient rounded up onto an integer (fixed by + 500).
+__device__ __forceinline__ double fmod500(double a) {
+    double m = a - floor(a / 500.0) * 500.0;
+    if (m < 0.0) m += 500.0;
+    return m;
+}
+
+// Schwefel term (CEC2022 schwefel_func), branch-free: with a = |z|,
+//   |z| <= 500:  -z sin(sqrt|z|)
+//   z  >  500:  -(500-m) sin(sqrt(500-m)) + ((z-500)/100)^2/n,  m = fmod(z, 500)
+//   z  < -500:  -(-500+m) sin(sqrt(500-m)) + ((z+500)/100)^2/n, m = fmod(|z|, 500)
+// are all -sign(z) s sin(sqrt s) (+ penalty) with s = a or 500 - m -- the same
+// roundings as the three-way form (oracle/cec_oracle.c), without divergence.
 __device__ __forceinline__ double schwefel_t(double zi, int n) {
-    if (zi > 500.0) {
-        const double m = fmod(zi, 500.0);
-        const double t = (zi - 500.0) / 100.0;
-        return -(500.0 - m) * sin(sqrt(500.0 - m)) + t * t / n;
-    }
-    if (zi < -500.0) {
-        const double m = fmod(fabs(zi), 500.0);
-        const double t = (zi + 500.0) / 100.0;
-        return -(-500.0 + m) * sin(sqrt(500.0 - m)) + t * t / n;
-    }
-    return -zi * sin(sqrt(fabs(zi)));
+    const double a = fabs(zi);
+    const bool out = a > 500.0;
+    const double s = out ? 500.0 - fmod500(a) : a;
+    const double v = s * sin(sqrt(s));
+    const double t = (zi > 0.0 ? zi - 500.0 : zi + 500.0) / 100.0;
+    return (zi > 0.0 ? -v : v) + (out ? t * t / n : 0.0);
 }
 
 // Basic function b over z[0..n) (shared memory, already scaled + offset).

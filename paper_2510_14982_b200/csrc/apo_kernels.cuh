@@ -510,9 +510,9 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     if (pf) {
         if (tile < ntiles) issue(tile, 0, sel_cur);
         cp_async_commit();
-        tile_nxt = claim();
-        sel_nxt = sel_of(tile_nxt);
     }
+    tile_nxt = tile < ntiles ? claim() : ntiles;
+    sel_nxt = sel_of(tile_nxt);
     int buf = 0;
     while (tile < ntiles) {
         const int r0 = A.row0 + tile * kCecRows;
@@ -539,8 +539,10 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         } else {
             issue(tile, 0, cur);
             cp_async_commit();
-            tile_next = claim();
-            sel_cur = sel_of(tile_next);
+            tile_next = tile_nxt;  // claimed one tile ahead: the atomic's latency hides behind this tile
+            tile_nxt = tile_next < ntiles ? claim() : ntiles;
+            sel_cur = sel_nxt;
+            sel_nxt = sel_of(tile_nxt);
             cp_async_wait_all();
         }
         __syncwarp();
