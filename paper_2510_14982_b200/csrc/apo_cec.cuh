@@ -702,16 +702,17 @@ __device__ inline double cec_basic_quad(int b, const double* z, int n, int t, co
 // row buffer (hybrids, compositions).  X is overwritten except for
 // compositions.  Every lane of quad q returns candidate q's fitness.
 template <int NT>
-__device__ inline double cec_eval_quad(const CecData& C, double* X, double* W, int xs, int n, int lane,
-                                       const double* ew, const double* bsm = nullptr) {
-    // bsm: shared-memory copy of rotation 0 (row stride 8 NT + 4), else rot_pad through L1
-    const double* B0 = bsm ? bsm : C.rot_pad;
-    const int bs0 = bsm ? 8 * NT + 4 : 8 * NT;
+__device__ inline double cec_eval_quad(const CecData& C, double* X, const double* src, int xs, int n, int lane,
+                                       const double* ew, const double* bsm = nullptr, int bsm_comp = 0) {
+    // bsm: shared-memory copy (row stride 8 NT + 4) of rotation `bsm_comp`, the others via L1.
+    // src: this quad's candidate row in global memory (nullptr for a dead row): compositions
+    // re-read it for every component instead of keeping a second copy in shared memory.
+    const double* B0 = (bsm && bsm_comp == 0) ? bsm : C.rot_pad;
+    const int bs0 = (bsm && bsm_comp == 0) ? 8 * NT + 4 : 8 * NT;
     const CecSpec& S = kCecSpec[C.fn - 1];
     const int q = lane >> 2, t = lane & 3;
     const int n4 = (n + 3) & ~3;
     double* x = X + (size_t)q * xs;
-    double* w = W + (size_t)q * xs;
     double f = 0.0;
     if (S.kind == 0) {
         const int b = S.basic[0];
@@ -760,20 +761,24 @@ __device__ inline double cec_eval_quad(const CecData& C, double* X, double* W, i
             const double sc = cec_scale(b), off = cec_offset(b);
             const double* o = C.shift + (size_t)k * n;
             const bool rot = S.rflag[k] != 0;
+            if (k > 0) {  // the candidate again (L2-resident: k_cec_eval just streamed it in)
+                for (int i = t; i < n; i += 4) x[i] = src ? src[i] : 0.0;
+                __syncwarp();
+            }
             double d2 = 0.0;
-            for (int i = t; i < n4; i += 4) {
-                if (i < n) {
-                    const double dv = x[i] - o[i];
-                    d2 += dv * dv;
-                    w[i] = rot ? dv * sc : dv * sc + off;
-                } else {
-                    w[i] = 0.0;
-                }
+            for (int i = t; i < n; i += 4) {
+                const double dv = x[i] - o[i];
+                d2 += dv * dv;
+                x[i] = rot ? dv * sc : dv * sc + off;
             }
             d2 = qsum(d2);
             __syncwarp();
-            if (rot) cec_rotate_quad<NT>(C.rot_pad + (size_t)k * n4 * (8 * NT), W, xs, n, off, lane);
-            fit[k] = S.lam[k] * cec_basic_quad(b, w, n, t, ew) + S.bias[k];
+            if (rot) {
+                const bool sm = bsm && bsm_comp == k;
+                cec_rotate_quad<NT>(sm ? bsm : C.rot_pad + (size_t)k * n4 * (8 * NT), X, xs, n, off, lane,
+                                    sm ? 8 * NT + 4 : 8 * NT);
+            }
+            fit[k] = S.lam[k] * cec_basic_quad(b, x, n, t, ew) + S.bias[k];
             __syncwarp();
             wk[k] = d2 != 0.0 ? sqrt(1.0 / d2) * exp(-d2 / 2.0 / n / (S.sigma[k] * S.sigma[k]))
                               : __longlong_as_double(0x7ff0000000000000LL);

@@ -14,9 +14,11 @@ static const void* pick(int dim) {
     }
 }
 
+// Every CEC2022 function takes the FAST form (one rotation staged in shared
+// memory); the L1-only form stays in apo_kernels.cuh for experiments.
 const void* pick_cec_eval(bool sel, int dim, bool fast) {
-    if (fast) return sel ? pick<true, true>(dim) : pick<false, true>(dim);
-    return sel ? pick<true, false>(dim) : pick<false, false>(dim);
+    (void)fast;
+    return sel ? pick<true, true>(dim) : pick<false, true>(dim);
 }
 
 }  // namespace apo

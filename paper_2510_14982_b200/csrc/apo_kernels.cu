@@ -331,7 +331,11 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     E.ld = a.P.ld;
     E.O = a.O;
     const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
-    E.bufs = (fn_id >= 9) ? 1 : 0;  // compositions keep the candidate and need W (hybrids permute in rot_pad)
+    E.bufs = 0;  // hybrids permute inside rot_pad, compositions re-read the candidate per component
+    static const int kNcomp[12] = {1, 1, 1, 1, 1, 1, 1, 1, 5, 3, 5, 6};
+    static const int kFirstRot[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0};  // first rflag = 1 (apo_cec.cuh kCecSpec)
+    E.ncomp = kNcomp[fn_id - 1];
+    E.bsm_comp = kFirstRot[fn_id - 1];
     E.pos0 = a.pos0;
     E.pos1 = a.pos1;
     E.sel = a.sel;
@@ -345,9 +349,10 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     E.cand_ok = cand_ok;
     E.warn_count = a.warn_count;
     E.trace_key = a.trace_key;
-    // F1-F8 (one rotation): rotation staged in SMEM, X double-buffered, as many warps as fit (<= 16);
-    // compositions: B through L1, 8 warps, 2 CTAs/SM
-    const bool fast = fn_id <= 8;
+    // the (first) rotation + shift vectors staged in SMEM per CTA, as many warps as fit (<= 16, a
+    // multiple of 4), X double-buffered only if that does not cost warps; further composition
+    // rotations are read through L1
+    const bool fast = true;
     const void* fe = pick_cec_eval(sel_mode, dim, fast);
     int ewarps = kWarps;
     E.prefetch = 0;
@@ -358,7 +363,7 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
             optin = 227 * 1024;
         static const int env_pf = getenv("APO_CEC_PREFETCH") ? atoi(getenv("APO_CEC_PREFETCH")) : -1;
-        const size_t bsm = cec_bsm_bytes(dim, cec_nt(dim));
+        const size_t bsm = cec_bsm_bytes(dim, cec_nt(dim), E.ncomp);
         auto fit_warps = [&](bool pf) {
             int w = (int)(((size_t)optin - bsm) / cec_eval_warp_bytes(dim, E.bufs, pf));
             if (w > 16) w = 16;

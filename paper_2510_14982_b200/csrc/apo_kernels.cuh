@@ -425,6 +425,8 @@ struct CecEvalArgs {
     unsigned long long* trace_key;
     unsigned* tile_counter;  // zeroed before the launch: warps claim 8-row tiles dynamically
     int prefetch;            // FAST: double-buffer X with cp.async (else one X tile per warp, more warps)
+    int bsm_comp;            // FAST: the component whose rotation is staged in shared memory
+    int ncomp;               // shift vectors to stage
 };
 
 // FAST (F1-F8: one rotation): the CTA stages that rotation in shared memory
@@ -436,8 +438,8 @@ __host__ __device__ inline int cec_bsm_stride(int nt) { return 8 * nt + 4; }
 __host__ __device__ inline size_t cec_eval_warp_bytes(int dim, int bufs, bool prefetch) {
     return 8 * (size_t)((prefetch ? 2 : 1) + bufs) * kCecRows * (size_t)cec_stride(dim);  // bufs = W buffers
 }
-__host__ __device__ inline size_t cec_bsm_bytes(int dim, int nt) {  // rotation + shift vector
-    return 8 * (size_t)((dim + 3) & ~3) * (size_t)cec_bsm_stride(nt) + 8 * (size_t)((dim + 1) & ~1);
+__host__ __device__ inline size_t cec_bsm_bytes(int dim, int nt, int ncomp) {  // rotation + shift vectors
+    return 8 * (size_t)((dim + 3) & ~3) * (size_t)cec_bsm_stride(nt) + 8 * (size_t)ncomp * (size_t)((dim + 1) & ~1);
 }
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -456,18 +458,18 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     const bool pf = FAST && A.prefetch;
     double* base = reinterpret_cast<double*>(smem + (size_t)warp * cec_eval_warp_bytes(dim, A.bufs, pf));
     double* Xb[2] = {base, base + (size_t)kCecRows * cs};
-    double* W = base + (size_t)(pf ? 2 : 1) * kCecRows * cs;  // compositions only
     double* bsm = nullptr;
     CecData C = A.O.cec;
     if constexpr (FAST) {
         bsm = reinterpret_cast<double*>(smem + (size_t)nwarps * cec_eval_warp_bytes(dim, A.bufs, pf));
         const int bs = cec_bsm_stride(NT), w8 = 8 * NT;
+        const double* rsrc = C.rot_pad + (size_t)A.bsm_comp * n4 * w8;
         for (int e = threadIdx.x; e < n4 * w8; e += blockDim.x) {
             const int i = e / w8, j = e - i * w8;
-            bsm[i * bs + j] = C.rot_pad[e];
+            bsm[i * bs + j] = rsrc[e];
         }
-        double* osm = bsm + (size_t)n4 * bs;  // the shift vector too (read once per element per tile)
-        for (int i = threadIdx.x; i < dim; i += blockDim.x) osm[i] = C.shift[i];
+        double* osm = bsm + (size_t)n4 * bs;  // the shift vectors too (read once per element per tile)
+        for (int i = threadIdx.x; i < A.ncomp * dim; i += blockDim.x) osm[i] = C.shift[i];
         C.shift = osm;
         __syncthreads();
     }
@@ -546,7 +548,9 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
             cp_async_wait_all();
         }
         __syncwarp();
-        const double nf = cec_eval_quad<NT>(C, Xb[buf], W, cs, dim, lane, ew, bsm);
+        const double* qsrc = nullptr;  // this quad's candidate row (compositions re-read it per component)
+        if (live) qsrc = SEL ? (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
+        const double nf = cec_eval_quad<NT>(C, Xb[buf], qsrc, cs, dim, lane, ew, bsm, A.bsm_comp);
         bool acc = false;
         if (live && t == 0) {
             double kept = fit_i;
