@@ -114,6 +114,8 @@ __host__ __device__ inline size_t group_head_bytes(int dim) {
 // loads of a DMMA (rows g = lane/4, columns t = lane%4) are bank-conflict
 // free.  cec_bufs = 0 (not CEC), 2 (F1-F8) or 3 (F9-F12).
 constexpr int kCecRows = 8;
+constexpr int kCecQuadMaxDim = 104;  // rot_pad exists for dim <= 104 (objectives.py, include/apo_b200.h)
+__host__ __device__ inline int cec_nt_dev(int n) { return n <= 16 ? 2 : n <= 32 ? 4 : n <= 56 ? 7 : 13; }
 __host__ __device__ inline int cec_stride(int dim) {
     const int s = (dim + 3) & ~3;
     return (s & 7) ? s : s + 4;
@@ -685,9 +687,33 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
         bool acc = false, warned = false;
         double cec_f = 0.0;
         if constexpr (KIND == KIND_ANY) {
-            if (cec)  // the batch's staged candidates together (DMMA rotation, apo_cec.cuh)
-                cec_f = cec_eval_batch(O.cec, g.T, g.T + (size_t)kCecRows * ts, g.T + (size_t)2 * kCecRows * ts, ts,
-                                       nb, P.dim, lane);
+            if (cec) {  // the batch's staged candidates together (DMMA rotation, apo_cec.cuh)
+                if (O.cec.rot_pad && P.dim <= kCecQuadMaxDim) {
+                    // quad-per-candidate evaluator (the k_cec_eval code): rows zero-padded to n4;
+                    // compositions re-read candidate q from the row it was written to
+                    const int q = lane >> 2, t4 = lane & 3, n4 = (P.dim + 3) & ~3;
+                    for (int i = P.dim + t4; i < n4; i += 4) g.T[(size_t)q * ts + i] = 0.0;
+                    const double* src = nullptr;
+                    if (q < nb) {
+                        const int own_key = g.slot[4 * (h + q)];
+                        if constexpr (MODE == OUT_SEL) src = R.alt_key(own_key);
+                        else src = out_rows + (size_t)(out_by_slot ? R.slot_of(own_key) : i0 - 1 + h + q) * P.ld;
+                    }
+                    __syncwarp();
+                    const double* ew = O.table_len >= P.dim ? O.table : nullptr;
+                    double fq;
+                    switch (cec_nt_dev(P.dim)) {
+                    case 2: fq = cec_eval_quad<2>(O.cec, g.T, src, ts, P.dim, lane, ew); break;
+                    case 4: fq = cec_eval_quad<4>(O.cec, g.T, src, ts, P.dim, lane, ew); break;
+                    case 7: fq = cec_eval_quad<7>(O.cec, g.T, src, ts, P.dim, lane, ew); break;
+                    default: fq = cec_eval_quad<13>(O.cec, g.T, src, ts, P.dim, lane, ew); break;
+                    }
+                    cec_f = __shfl_sync(kFull, fq, (lane & 7) * 4);  // lane q < 8 <- quad q
+                } else {
+                    cec_f = cec_eval_batch(O.cec, g.T, g.T + (size_t)kCecRows * ts, g.T + (size_t)2 * kCecRows * ts,
+                                           ts, nb, P.dim, lane);
+                }
+            }
         }
         if (lane < nb) {
             const int p = h + lane, i = i0 + p;

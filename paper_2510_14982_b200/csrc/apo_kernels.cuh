@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
 // rewritten with the old row).
 constexpr int kCecEvalMaxDim = 104;  // 13 register-resident n-tiles
 // n-tiles per rotation in k_cec_eval (rot_pad rows are 8 * cec_nt(n) wide)
-__host__ __device__ inline int cec_nt(int n) { return n <= 16 ? 2 : n <= 32 ? 4 : n <= 56 ? 7 : 13; }
+__host__ __device__ inline int cec_nt(int n) { return cec_nt_dev(n); }
 struct CecEvalArgs {
     int n_rows, dim, ld, bufs;
     int row0;          // first row (dense: rank) of the range
