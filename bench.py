@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c4", "c2", "c3"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2", "c3", "c5"])
     ap.add_argument("--objective", default="cec2022_f6")
     ap.add_argument("--ps", type=int, default=1_000_000)
     ap.add_argument("--dim", type=int, default=100)
@@ -320,6 +320,7 @@ def bench_ours(args, rank, world, local):
     if not args.no_suite and rank == 0:
         result["suite_c2"] = bench_suite(world)
         result["suite_c3"] = bench_c3()
+        result["suite_c5"] = bench_c5()
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(m["cfg"], args.objective)
     return result
@@ -459,6 +460,52 @@ def bench_c3():
             "best": best, "prefix_tables": "shared memory (k_run_batch stages the 515-entry table per CTA)"}
 
 
+def bench_c5(sizes=(10, 20, 50, 100, 1000), fns=(1, 4, 10), ps=10_000, iters=20, small=False):
+    """BASELINE config 5: dimension sweep on rotated functions, DMMA (tensor-core) rotation vs the FMA
+    path.  ps=10^4 device-resident loop (the paper's PS), `iters` timed iterations after 3 warm-up; with
+    small=True also ps=100 x 30 seeds x 200 iterations (one CTA per run where it fits in SMEM)."""
+    import torch
+
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200.engine import DeviceRun
+
+    rows = []
+    for fn in fns:
+        for dim in sizes:
+            for rot in (("dmma", "fma") if dim <= 104 else ("fma",)):
+                obj = pz.cec2022_objective(fn, rotation=rot)
+                cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=iters + 3)
+                run = DeviceRun(cfg, obj)
+                run.initialize()
+                run.iterate(3)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run.iterate(iters)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / iters
+                run.close()
+                row = {"fn": fn, "dim": dim, "ps": ps, "rotation": rot, "ms_per_iteration": round(ms, 4),
+                       "evals_per_s": ps / (ms / 1e3), "rotation_tflops": ps * 2.0 * dim * dim *
+                       {9: 3, 10: 1, 11: 5, 12: 6}.get(fn, 1) / (ms / 1e3) / 1e12}
+                if small:
+                    scfg = pz.ApoConfig(ps=100, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=200)
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    if pz.engine._batch_fits(scfg, [obj]):
+                        pz.run_batch(scfg, [obj] * 30, list(range(30)), want_trace=False, device_out=True)
+                    else:
+                        for sd in range(30):
+                            pz.run(pz.ApoConfig(ps=100, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim),
+                                                max_iterations=200, seed=sd), obj)
+                    torch.cuda.synchronize()
+                    row["ps100_30seeds_evals_per_s"] = 30 * 100 * 200 / (time.perf_counter() - t0)
+                rows.append(row)
+    return {"workload": f"C5: F{'/F'.join(str(f) for f in fns)} x D in {list(sizes)}, ps={ps}, DMMA vs FMA rotation",
+            "rows": rows}
+
+
 def cpu_baseline(cfg, objective, max_seconds=25.0):
     """The oracle's reference iteration (oracle.step, bit-identical to the reference) on all host cores."""
     import oracle
@@ -539,11 +586,12 @@ def main():
             print(json.dumps(res), flush=True)
         return
     rank, world, local = dist_setup("nccl")
-    if args.workload in ("c2", "c3"):
+    if args.workload in ("c2", "c3", "c5"):
         import torch
 
         torch.cuda.set_device(local)
-        res = bench_suite(world) if args.workload == "c2" else bench_c3()
+        res = (bench_suite(world) if args.workload == "c2" else bench_c3() if args.workload == "c3"
+               else bench_c5(small=True))
         if rank == 0:
             print(json.dumps({"metric": METRIC, **res, "n_gpus": world, "steps": 1, "warmup": 1}), flush=True)
         return

@@ -215,8 +215,10 @@ int apo_run_batch(int64_t nruns, const uint64_t *seeds, const apo_objective *obj
                   double upper, double eps, const double *sched, const double *p_dr, double *best_fit,
                   double *best_pos, double *trace, double *final_pos, double *final_fit, int64_t *warnings,
                   int rng, void *stream);
-/* Largest ps*dim the batch kernel can hold in shared memory. */
+/* Largest ps*dim the batch kernel can hold in shared memory (basic objectives). */
 int64_t apo_run_batch_max_elems(int64_t ps, int64_t dim);
+/* 1 if a batch of these objectives at (ps, dim) fits the shared-memory batch kernel. */
+int apo_run_batch_fits(int64_t ps, int64_t dim, const apo_objective *objectives_host, int64_t nobj);
 
 /* Host-side RNG entry points (no device needed; the kernels use the same
  * code): one Philox4x32-10 block, and the draw u(seed, iteration, individual,

@@ -64,6 +64,9 @@ class CecFunction:
 
     fn: int
     data_seed: int = 2022
+    # "dmma": tensor-core rotation (k_cec_eval / quad evaluator, dim <= 104);
+    # "fma": lane-per-output FMA rotation through L1 (BASELINE config 5's comparison path)
+    rotation: str = "dmma"
 
     def arrays(self, dim: int):
         return cec_data(self.fn, dim, self.data_seed)
@@ -80,12 +83,17 @@ class CecFunction:
 MIN_DIM = (2, 2, 2, 2, 2, 2, 5, 5, 2, 2, 2, 2)
 
 
-def cec2022_objective(fn: int, data_seed: int = 2022) -> Objective:
-    return Objective(f"cec2022_f{fn}", CEC2022_BASE + fn, min_dim=MIN_DIM[fn - 1], data=CecFunction(fn, data_seed))
+def cec2022_objective(fn: int, data_seed: int = 2022, rotation: str = "dmma") -> Objective:
+    if rotation not in ("dmma", "fma"):
+        raise ValueError(f"rotation must be 'dmma' or 'fma', got {rotation!r}")
+    name = f"cec2022_f{fn}" + ("" if rotation == "dmma" else "_fma")
+    return Objective(name, CEC2022_BASE + fn, min_dim=MIN_DIM[fn - 1], data=CecFunction(fn, data_seed, rotation))
 
 
 def _resolve(name: str):
     key = name.strip().lower()
+    if key.startswith("cec2022_f") and key.endswith("_fma") and key[9:-4].isdigit() and 1 <= int(key[9:-4]) <= 12:
+        return cec2022_objective(int(key[9:-4]), rotation="fma")
     for prefix in ("cec2022_f", "cec2022-f", "f"):
         if key.startswith(prefix) and key[len(prefix):].isdigit():
             k = int(key[len(prefix):])

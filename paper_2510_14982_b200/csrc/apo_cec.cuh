@@ -370,8 +370,8 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
 // Z[q][j] = sum_i rot_t[i][j] * Y[q][i] + off, q < 8 (rows are independent:
 // rows past the batch hold stale but harmless values).
 __device__ inline void cec_rotate8(const double* __restrict__ rot_t, const double* Y, double* Z, int ys, int n,
-                                   double off, int lane) {
-    if (n >= APO_CEC_DMMA_MIN_DIM) {
+                                   double off, int lane, bool dmma = true) {
+    if (dmma && n >= APO_CEC_DMMA_MIN_DIM) {
         const int g = lane >> 2, t = lane & 3;
         const double* yrow = Y + (size_t)g * ys;
         for (int j0 = 0; j0 < n; j0 += 16) {
@@ -418,6 +418,7 @@ __device__ inline void cec_rotate8(const double* __restrict__ rot_t, const doubl
 __device__ inline double cec_eval_batch(const CecData& C, double* X, double* Z, double* W, int xs, int nb, int n,
                                         int lane) {
     const CecSpec& S = kCecSpec[C.fn - 1];
+    const bool dmma = C.rot_pad != nullptr;  // objectives built without DMMA tables: FMA rotation
     double mine = 0.0;
     if (S.kind == 0) {
         const int b = S.basic[0];
@@ -432,7 +433,7 @@ __device__ inline double cec_eval_batch(const CecData& C, double* X, double* Z, 
             }
         }
         __syncwarp();
-        cec_rotate8(C.rot_t, X, Z, xs, n, cec_offset(b), lane);
+        cec_rotate8(C.rot_t, X, Z, xs, n, cec_offset(b), lane, dmma);
         __syncwarp();
         for (int q = 0; q < nb; q++) {
             const double v = cec_basic_warp(b, Z + (size_t)q * xs, n, lane);
@@ -444,7 +445,7 @@ __device__ inline double cec_eval_batch(const CecData& C, double* X, double* Z, 
             for (int i = lane; i < n; i += 32) x[i] = x[i] - C.shift[i];
         }
         __syncwarp();
-        cec_rotate8(C.rot_t, X, Z, xs, n, 0.0, lane);
+        cec_rotate8(C.rot_t, X, Z, xs, n, 0.0, lane, dmma);
         __syncwarp();
         int sizes[6];
         int tot = 0;
@@ -498,7 +499,7 @@ __device__ inline double cec_eval_batch(const CecData& C, double* X, double* Z, 
                 if (lane == q) d2_mine = d2;
             }
             __syncwarp();
-            if (S.rflag[k]) cec_rotate8(C.rot_t + (size_t)k * n * n, W, Z, xs, n, off, lane);
+            if (S.rflag[k]) cec_rotate8(C.rot_t + (size_t)k * n * n, W, Z, xs, n, off, lane, dmma);
             __syncwarp();
             double fk = 0.0;
             for (int q = 0; q < nb; q++) {

@@ -428,6 +428,26 @@ int dr_device(int rng, uint64_t seed, uint64_t key_iteration, int64_t ps, int64_
     return APO_OK;
 }
 
+int smem_optin() {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
+    return optin;
+}
+
+// Shared-memory extras of a batch: CEC2022 scratch rows (one X tile when the quad evaluator can
+// run -- rot_pad present, dim <= 104 -- else the fallback's 2-3 buffers) and threshold tables.
+void batch_smem_needs(const apo_objective* objs, int64_t n, int64_t dim, int* cec_bufs, int* tab_smem) {
+    *cec_bufs = 0;
+    *tab_smem = 0;
+    for (int64_t k = 0; k < n; k++) {
+        int cb = cec_bufs_for(objs[k].code);
+        if (cb > 0 && objs[k].rot_pad && dim <= kCecQuadMaxDim) cb = 1;
+        if (cb > *cec_bufs) *cec_bufs = cb;
+        if (objs[k].code == APO_OBJ_OTSU_ML || objs[k].code == APO_OBJ_KAPUR_ML) *tab_smem = APO_THRESHOLD_TABLE_LEN;
+    }
+}
+
 size_t dr_tmp_bytes(int64_t cap, int64_t ps) {
     size_t b = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, b, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
@@ -1166,6 +1186,14 @@ int apo_shard_destroy(apo_shard* r) {
 
 // ------------------------------ batched runs -------------------------------
 
+int apo_run_batch_fits(int64_t ps, int64_t dim, const apo_objective* objectives_host, int64_t nobj) {
+    if (ps < 1 || dim < 1 || dim > 8192 || !objectives_host || nobj < 1) return 0;
+    int cec_bufs = 0, tab = 0;
+    batch_smem_needs(objectives_host, nobj, dim, &cec_bufs, &tab);
+    const BatchLayout L = batch_layout((int)ps, (int)dim, (int)((dim + 1) & ~1LL), kWarps, cec_bufs, tab);
+    return (int64_t)L.total + 2048 <= smem_optin() ? 1 : 0;
+}
+
 int64_t apo_run_batch_max_elems(int64_t ps, int64_t dim) {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
@@ -1218,21 +1246,9 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     A.final_fit = final_fit;
     A.warnings = (long long*)warnings;
     A.rng = rng;
-    A.cec_bufs = 0;
-    A.tab_smem = 0;
-    for (int64_t k = 0; k < nruns; k++) {
-        const int cb = cec_bufs_for(objectives_host[k].code);
-        if (cb > A.cec_bufs) A.cec_bufs = cb;
-        if (objectives_host[k].code == APO_OBJ_OTSU_ML || objectives_host[k].code == APO_OBJ_KAPUR_ML)
-            A.tab_smem = APO_THRESHOLD_TABLE_LEN;
-    }
+    batch_smem_needs(objectives_host, nruns, dim, &A.cec_bufs, &A.tab_smem);
     const BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs, A.tab_smem);
-    {
-        int dev = 0, optin = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
-        APO_CHECK((int64_t)L.total + 2048 <= optin, "population too large for the shared-memory batch kernel");
-    }
+    APO_CHECK((int64_t)L.total + 2048 <= smem_optin(), "population too large for the shared-memory batch kernel");
     const void* fn = pick_run_batch((int)dim);
     if (int rc = set_smem(fn, L.total)) return rc;
     void* args[] = {(void*)&A};

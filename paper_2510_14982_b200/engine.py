@@ -273,8 +273,16 @@ def rng_code(cfg: ApoConfig) -> int:
     return 1 if cfg.rng == "philox" else 0
 
 
-def _batch_fits(cfg: ApoConfig) -> bool:
-    return int(_lib.require_cuda().apo_run_batch_max_elems(cfg.ps, cfg.dim)) > 0
+def _batch_fits(cfg: ApoConfig, objectives=()) -> bool:
+    """Whether (ps, dim) and these objectives fit the shared-memory batch kernel."""
+    lib = _lib.require_cuda()
+    objs = [resolve_objective(o) for o in objectives]
+    if not objs:
+        return int(lib.apo_run_batch_max_elems(cfg.ps, cfg.dim)) > 0
+    descs = (_lib.apo_objective * len(objs))()
+    for k, o in enumerate(objs):
+        descs[k] = device_objective(o, cfg.dim).struct
+    return bool(lib.apo_run_batch_fits(cfg.ps, cfg.dim, descs, len(objs)))
 
 
 def run(cfg: ApoConfig, objective, mode: Optional[EngineMode] = None, backend: Optional[str] = None) -> RunResult:
@@ -286,7 +294,7 @@ def run(cfg: ApoConfig, objective, mode: Optional[EngineMode] = None, backend: O
     _check(cfg, obj)
     n_iters = cfg.iterations_within_budget()
     started = time.perf_counter()
-    if cfg.ps <= BATCH_PS_LIMIT and _batch_fits(cfg):
+    if cfg.ps <= BATCH_PS_LIMIT and _batch_fits(cfg, [obj]):
         b = run_batch(cfg, [obj], [cfg.seed], want_population=True)
         seconds = time.perf_counter() - started
         return RunResult(best_position=b.best_position[0], best_fitness=float(b.best_fitness[0]), trace=b.trace[0],
@@ -338,7 +346,7 @@ def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_t
         raise ValueError("one objective per seed")
     for o in objs:
         _check(cfg, o)
-    if not _batch_fits(cfg):
+    if not _batch_fits(cfg, list({id(o): o for o in objs}.values())):
         raise ValueError(f"ps*dim = {cfg.ps * cfg.dim} does not fit the shared-memory batch kernel")
     n = len(objs)
     dev = _dev()

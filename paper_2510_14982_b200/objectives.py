@@ -172,7 +172,8 @@ class DeviceObjective:
             shift, rot, shuffle = obj.data.arrays(dim)
             rot_t = np.ascontiguousarray(np.transpose(rot, (0, 2, 1)))
             arrays = [("shift", shift), ("rot_t", rot_t), ("shuffle", shuffle)]
-            if dim <= 104:  # zero-padded M^T for the DMMA evaluation kernel (include/apo_b200.h)
+            if dim <= 104 and getattr(obj.data, "rotation", "dmma") == "dmma":
+                # zero-padded M^T for the DMMA evaluation kernel (include/apo_b200.h)
                 nt = 2 if dim <= 16 else 4 if dim <= 32 else 7 if dim <= 56 else 13
                 n4 = (dim + 3) // 4 * 4
                 pad = np.zeros((rot_t.shape[0], n4, 8 * nt))

@@ -114,3 +114,27 @@ def test_suite_batch_matches_oracle_runs():
     rel = np.abs(res.best_fitness - want) / np.abs(want)
     assert np.mean(rel <= 1e-9) >= 0.8
     assert np.all(rel <= 1e-2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fn", [1, 4, 6, 10])
+def test_fma_rotation_path_matches_oracle(fn):
+    """BASELINE config 5's comparison path: the same objective without DMMA tables rotates with
+    lane-per-output FMAs (fused update kernel); it must agree with the oracle like the DMMA path."""
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200.kernels import get_backend
+
+    name = f"cec2022_f{fn}"
+    ps, dim = 1500, 50
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=50, seed=fn)
+    pos, fit = oracle.initialize(fn, ps, dim, -100.0, 100.0, name)
+    order = oracle.argsort_stable(fit)
+    sp, sf = pos[order], fit[order]
+    in_dr = oracle.select_dr(fn, 4, ps, 0.1)
+    want = oracle.run_updates(sp, sf, in_dr, seed=fn, iteration=3, max_iterations=50, name=name,
+                              lower=-100.0, upper=100.0, nthreads=8)
+    for rot in ("fma", "dmma"):
+        got = get_backend("cuda").run_updates(sp, sf, in_dr, cfg, pz.cec2022_objective(fn, rotation=rot), 3, 4)
+        agree = got[2] == want[2]
+        assert agree.mean() > 0.99, rot
+        np.testing.assert_allclose(got[1][agree], want[1][agree], rtol=RTOL)

@@ -216,3 +216,40 @@ def test_histogram_and_threshold(pz):
     res = pz.apo_threshold(img, ps=100, iterations=50, seed=0)
     assert res.threshold == int(g["apo_t"]) and res.variance == float(g["apo_var"])
     assert np.array_equal(res.run.trace, g["apo_trace"])
+
+
+def _random_configs(n, seed=2026):
+    """The reference's acceptance criterion 2 draws 200 random configurations (test_acceptance.py:
+    183-205); here each one runs on the GPU and must equal the oracle run bit for bit."""
+    rnd = np.random.default_rng(seed)
+    names = ["sphere", "bent_cigar", "high_conditioned_elliptic", "hgbat", "rosenbrock"]
+    out = []
+    for k in range(n):
+        ps = int(rnd.choice([2, 3, 7, 33, 64, 100, 257, 700, 1500]))
+        dim = int(rnd.choice([1, 2, 5, 17, 32, 33, 64, 100, 129, 300]))
+        name = names[k % len(names)]
+        if name in ("high_conditioned_elliptic", "rosenbrock") and dim < 2:
+            dim = 2
+        lo = float(rnd.uniform(-50, 0))
+        hi = lo + float(rnd.uniform(0.5, 80))
+        npairs = int(rnd.integers(1, min(ps - 1, 4) + 1)) if ps > 1 else 1
+        out.append(dict(ps=ps, dim=dim, name=name, lo=lo, hi=hi, T=int(rnd.integers(1, 12)),
+                        seed=int(rnd.integers(0, 2 ** 63)), npairs=npairs, pf_max=float(rnd.uniform(0.05, 1.0))))
+    return out
+
+
+@pytest.mark.parametrize("c", _random_configs(40), ids=lambda c: f"{c['name']}-{c['ps']}x{c['dim']}")
+def test_random_configurations_bit_exact(pz, c, monkeypatch):
+    from paper_2510_14982_b200 import engine
+
+    want = oracle.run(ps=c["ps"], dim=c["dim"], max_iterations=c["T"], seed=c["seed"], name=c["name"],
+                      lower=c["lo"], upper=c["hi"], npairs=c["npairs"], pf_max=c["pf_max"], nthreads=8)
+    cfg = pz.ApoConfig(ps=c["ps"], dim=c["dim"], bounds=pz.Bounds(c["lo"], c["hi"], c["dim"]),
+                       max_iterations=c["T"], seed=c["seed"], neighbor_pairs=c["npairs"], pf_max=c["pf_max"])
+    for limit in (engine.BATCH_PS_LIMIT, 0):  # one-CTA batch kernel (when it fits) and the HBM device loop
+        monkeypatch.setattr(engine, "BATCH_PS_LIMIT", limit)
+        res = pz.run(cfg, c["name"])
+        assert np.array_equal(res.trace, want["trace"])
+        assert np.array_equal(res.population.positions, want["positions"])
+        assert np.array_equal(res.population.fitness, want["fitness"])
+        assert res.warnings == want["warnings"] and res.best_fitness == want["best_fitness"]
