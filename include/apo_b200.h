@@ -78,6 +78,11 @@ typedef struct apo_objective {
      * For the hybrids (F6-F8) its output columns are permuted by the
      * shuffle: rot_pad[0][i][j] = rot_t[0][i][shuffle[j]-1]. */
     const double *rot_pad;
+    /* CEC2022 F1-F8 and F10 at dim > 104, optional: the rotated component's
+     * rot_t zero-padded to [round_up(dim,16)][round_up(dim,64)] (hybrids: columns
+     * permuted like rot_pad).  When present, the device loop rotates all
+     * candidates of an iteration as one DMMA GEMM (apo_cec_gemm.cu). */
+    const double *rot_gemm;
 } apo_objective;
 
 int apo_abi_version(void);

@@ -13,6 +13,7 @@ import os
 import shutil
 import subprocess
 import threading
+import time
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG_DIR)
@@ -26,7 +27,9 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-
               "-diag-suppress", "177"]
 # One TU per kernel family so nvcc runs in parallel (the templates live in
 # csrc/apo_kernels.cuh); linked into a single shared library.
-SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_batch.cu", "apo_cec_eval.cu"]
+SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_batch.cu", "apo_batch_m1.cu",
+           "apo_batch_m2.cu", "apo_batch_m4.cu", "apo_batch_m0.cu", "apo_batch_warp.cu", "apo_cec_eval.cu",
+           "apo_cec_gemm.cu"]
 
 _lock = threading.Lock()
 _lib = None
@@ -70,7 +73,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = [nvcc(), *ARCH_FLAGS, *flags, "-I", INCLUDE, "-I", CSRC, "-c", "-o", obj, os.path.join(CSRC, src)]
             if verbose:
                 print(" ".join(cmd), flush=True)
-            return obj, subprocess.run(cmd, capture_output=True, text=True)
+            t0 = time.time()
+            proc = subprocess.run(cmd, capture_output=True, text=True)
+            if verbose:
+                print(f"  {src}: {time.time() - t0:.0f} s", flush=True)
+            return obj, proc
 
         with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
             results = list(ex.map(compile_one, SOURCES))
@@ -95,7 +102,8 @@ _INT = C.c_int
 
 class apo_objective(C.Structure):
     _fields_ = [("code", C.c_int32), ("table_len", C.c_int32), ("table", C.c_void_p), ("shift", C.c_void_p),
-                ("rot_t", C.c_void_p), ("shuffle", C.c_void_p), ("rot_pad", C.c_void_p)]
+                ("rot_t", C.c_void_p), ("shuffle", C.c_void_p), ("rot_pad", C.c_void_p),
+                ("rot_gemm", C.c_void_p)]
 
 
 PROTOTYPES = {

@@ -1,14 +1,21 @@
-// apo_batch.cu -- instantiates the persistent one-CTA-per-run batch kernel.
+// apo_batch.cu -- picks the persistent one-CTA-per-run batch kernel; each
+// MAXC variant is instantiated in its own TU (apo_batch_m*.cu) so they build in parallel.
 #include "apo_kernels.cuh"
 
 namespace apo {
 
+const void* batch_kernel_m1();
+const void* batch_kernel_m2();
+const void* batch_kernel_m4();
+const void* batch_kernel_m0();
+const void* batch_kernel_warp();
+
 const void* pick_run_batch(int dim) {
-    if (dim <= 32) return (const void*)k_run_batch<1>;
-    if (dim <= 64) return (const void*)k_run_batch<2>;
-    if (dim <= 128) return (const void*)k_run_batch<4>;
-    if (dim <= kGroupMaxDim) return (const void*)k_run_batch<0>;
-    return (const void*)k_run_batch<-1>;
+    if (dim <= 32) return batch_kernel_m1();
+    if (dim <= 64) return batch_kernel_m2();
+    if (dim <= 128) return batch_kernel_m4();
+    if (dim <= kGroupMaxDim) return batch_kernel_m0();
+    return batch_kernel_warp();
 }
 
 }  // namespace apo

@@ -260,6 +260,7 @@ struct CecData {
     const double* rot_t;    // [ncomp][n][n]
     const int* shuffle;     // [n] (1-based)
     const double* rot_pad;  // [ncomp][n4][8 NT] zero-padded rot_t (k_cec_eval), nullable
+    const double* rot_gemm;  // [Kp][Np] zero-padded rot_t of the rotated component (D > 104 GEMM path), nullable
 };
 
 // F_fn(c) for a candidate c[0..n) in shared memory; y, z: shared scratch [n].

@@ -688,7 +688,7 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
         double cec_f = 0.0;
         if constexpr (KIND == KIND_ANY) {
             if (cec) {  // the batch's staged candidates together (DMMA rotation, apo_cec.cuh)
-                if (O.cec.rot_pad && P.dim <= kCecQuadMaxDim) {
+                if (MAXC > 0 && O.cec.rot_pad && P.dim <= kCecQuadMaxDim) {
                     // quad-per-candidate evaluator (the k_cec_eval code): rows zero-padded to n4;
                     // compositions re-read candidate q from the row it was written to
                     const int q = lane >> 2, t4 = lane & 3, n4 = (P.dim + 3) & ~3;
@@ -701,12 +701,17 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
                     }
                     __syncwarp();
                     const double* ew = O.table_len >= P.dim ? O.table : nullptr;
-                    double fq;
-                    switch (cec_nt_dev(P.dim)) {
-                    case 2: fq = cec_eval_quad<2>(O.cec, g.T, src, ts, P.dim, lane, ew); break;
-                    case 4: fq = cec_eval_quad<4>(O.cec, g.T, src, ts, P.dim, lane, ew); break;
-                    case 7: fq = cec_eval_quad<7>(O.cec, g.T, src, ts, P.dim, lane, ew); break;
-                    default: fq = cec_eval_quad<13>(O.cec, g.T, src, ts, P.dim, lane, ew); break;
+                    // the n-tile counts a register-resident variant can meet (MAXC bounds dim)
+                    double fq = 0.0;
+                    const int nt = cec_nt_dev(P.dim);
+                    if constexpr (MAXC == 1) {
+                        fq = nt == 2 ? cec_eval_quad<2>(O.cec, g.T, src, ts, P.dim, lane, ew)
+                                     : cec_eval_quad<4>(O.cec, g.T, src, ts, P.dim, lane, ew);
+                    } else if constexpr (MAXC == 2) {
+                        fq = nt == 7 ? cec_eval_quad<7>(O.cec, g.T, src, ts, P.dim, lane, ew)
+                                     : cec_eval_quad<13>(O.cec, g.T, src, ts, P.dim, lane, ew);
+                    } else if constexpr (MAXC == 4) {
+                        fq = cec_eval_quad<13>(O.cec, g.T, src, ts, P.dim, lane, ew);
                     }
                     cec_f = __shfl_sync(kFull, fq, (lane & 7) * 4);  // lane q < 8 <- quad q
                 } else {

@@ -88,6 +88,7 @@ ObjDesc to_desc(const apo_objective* o) {
     d.cec.rot_t = o->rot_t;
     d.cec.shuffle = o->shuffle;
     d.cec.rot_pad = o->rot_pad;
+    d.cec.rot_gemm = o->rot_gemm;
     return d;
 }
 
@@ -288,26 +289,40 @@ __global__ void k_debug_exp(const double* x, double* out, long long n) {
 
 
 
+int smem_optin() {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
+    return optin;
+}
+
 // Fused update launch.  CEC2022 objectives with dim <= kCecEvalMaxDim and a
 // cand_ok scratch run as two kernels: k_update_group writes the candidates,
 // k_cec_eval evaluates them in DMMA tiles and finishes the update.
 // mid_event (nullable) is recorded between the two.
+
 int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* cand_ok = nullptr,
                   cudaEvent_t mid_event = nullptr, unsigned* tile_counter = nullptr) {
     UpdArgs a = A0;
     const int dim = a.P.dim;
     const bool group = dim <= kGroupMaxDim;
+    const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
     const bool split = group && cand_ok && a.O.code > APO_OBJ_CEC2022_BASE && dim <= kCecEvalMaxDim &&
                        a.O.cec.rot_pad != nullptr;
-    if (split) {
+    // D > 104: candidates, then the rotation of every candidate as one DMMA GEMM (apo_cec_gemm.cu)
+    const bool gemm = !split && cand_ok && a.O.code > APO_OBJ_CEC2022_BASE && dim > kCecEvalMaxDim &&
+                      a.O.cec.rot_gemm != nullptr && (fn_id <= 8 || fn_id == 10);
+    if (split || gemm) {
         a.cand_ok = cand_ok;
         a.cec_bufs = 0;
     }
-    const int w = group ? kWarps : warps_for_dim(dim);
+    int w = group ? kWarps : warps_for_dim(dim);
     const bool stage = sel_mode && dim <= APO_STAGE_MAX_DIM;
-    const size_t smem = (group ? group_scratch_bytes(dim, stage, a.cec_bufs) : warp_scratch_bytes(dim)) * (size_t)w;
+    const size_t per_warp = group ? group_scratch_bytes(dim, stage, a.cec_bufs) : warp_scratch_bytes(dim);
+    while (w > 1 && per_warp * (size_t)w + 1024 > (size_t)smem_optin()) w--;  // e.g. fused CEC at D ~ 150-256
+    const size_t smem = per_warp * (size_t)w;
     const bool cec = a.O.code > APO_OBJ_CEC2022_BASE;
-    const void* fn = sel_mode ? pick_update_sel(dim, split, cec) : pick_update_dense(dim, split, cec);
+    const void* fn = sel_mode ? pick_update_sel(dim, split || gemm, cec) : pick_update_dense(dim, split || gemm, cec);
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
@@ -322,6 +337,34 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         APO_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(32 * w), args, smem, st));
     }
     if (mid_event) APO_CUDA(cudaEventRecord(mid_event, st));
+    if (gemm) {
+        CecGemmArgs G{};
+        G.row0 = a.rank_lo;
+        G.n_rows = a.rank_hi - a.rank_lo;
+        G.dim = dim;
+        G.ld = a.P.ld;
+        G.kp = gemm_kp(dim);
+        G.np = gemm_np(dim);
+        G.comp = fn_id == 10 ? 1 : 0;  // F10: the one rotated component (kCecSpec rflag {0, 1, 0})
+        G.O = a.O;
+        G.pos0 = a.pos0;
+        G.pos1 = a.pos1;
+        G.sel = sel_mode ? a.sel : nullptr;
+        G.sel_next = a.sel_next;
+        G.pos = a.pos;
+        G.out_pos = a.out_pos;
+        G.order = sel_mode ? nullptr : a.order;
+        G.out_acc = a.out_acc;
+        G.out_warn = a.out_warn;
+        G.fit = a.fit;
+        G.out_fit = a.out_fit;
+        G.cand_ok = cand_ok;
+        G.warn_count = a.warn_count;
+        G.trace_key = a.trace_key;
+        const int rc = cec_gemm_finish(G, st, num_sms());
+        if (rc) return fail(APO_ECUDA, "cec_gemm_finish failed");
+        return APO_OK;
+    }
     if (!split) return APO_OK;
     CecEvalArgs E{};
     E.row0 = a.rank_lo;
@@ -330,7 +373,6 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     E.dim = dim;
     E.ld = a.P.ld;
     E.O = a.O;
-    const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
     E.bufs = 0;  // hybrids permute inside rot_pad, compositions re-read the candidate per component
     static const int kNcomp[12] = {1, 1, 1, 1, 1, 1, 1, 1, 5, 3, 5, 6};
     static const int kFirstRot[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0};  // first rflag = 1 (apo_cec.cuh kCecSpec)
@@ -428,12 +470,6 @@ int dr_device(int rng, uint64_t seed, uint64_t key_iteration, int64_t ps, int64_
     return APO_OK;
 }
 
-int smem_optin() {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
-    return optin;
-}
 
 // Shared-memory extras of a batch: CEC2022 scratch rows (one X tile when the quad evaluator can
 // run -- rot_pad present, dim <= 104 -- else the fallback's 2-3 buffers) and threshold tables.

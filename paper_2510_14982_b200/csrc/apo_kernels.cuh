@@ -84,23 +84,33 @@ __global__ void __launch_bounds__(kThreads) k_update(UpdArgs A) {
         const bool dr = A.in_dr_bits ? ((A.in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0 : A.in_dr_bytes[r0] != 0;
         const double pdr = dr ? A.p_dr[r0] : 0.0;
         UpdateResult res;
+        const bool co = A.cand_ok != nullptr;  // candidates only (CEC2022 large-D GEMM path)
         if constexpr (SEL) {
             const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
             const int slot = A.order[r0];
-            res = update_protozoon(P, A.O, R, r0 + 1, dr, pdr, R.alt(slot), s, lane);
+            res = update_protozoon(P, A.O, R, r0 + 1, dr, pdr, R.alt(slot), s, lane, co);
             if (lane == 0) {
-                A.out_fit[slot] = res.fitness;
-                A.sel_next[slot] = A.sel[slot] ^ 1;  // the full kept row went to the alternate buffer
+                if (co) {
+                    A.cand_ok[slot] = res.accepted ? 1 : 0;
+                } else {
+                    A.out_fit[slot] = res.fitness;
+                    A.sel_next[slot] = A.sel[slot] ^ 1;  // the full kept row went to the alternate buffer
+                }
             }
         } else {
             const DenseRows R{A.pos, A.fit, P.ld};
-            res = update_protozoon(P, A.O, R, r0 + 1, dr, pdr, A.out_pos + (size_t)r0 * P.ld, s, lane);
+            res = update_protozoon(P, A.O, R, r0 + 1, dr, pdr, A.out_pos + (size_t)r0 * P.ld, s, lane, co);
             if (lane == 0) {
-                A.out_fit[r0] = res.fitness;
-                if (A.out_acc) A.out_acc[r0] = res.accepted ? 1 : 0;
-                if (A.out_warn) A.out_warn[r0] = res.warned ? 1 : 0;
+                if (co) {
+                    A.cand_ok[r0] = res.accepted ? 1 : 0;
+                } else {
+                    A.out_fit[r0] = res.fitness;
+                    if (A.out_acc) A.out_acc[r0] = res.accepted ? 1 : 0;
+                    if (A.out_warn) A.out_warn[r0] = res.warned ? 1 : 0;
+                }
             }
         }
+        if (co) continue;
         if (lane == 0) {
             const unsigned long long k = sort_key(res.fitness);
             my_min = k < my_min ? k : my_min;
@@ -590,6 +600,31 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     cp_async_wait_all();
     block_finish(my_min, my_warn, A.warn_count, A.trace_key);
 }
+
+// CEC2022 at D > kCecEvalMaxDim: transform -> DMMA GEMM -> finish (apo_cec_gemm.cu).
+struct CecGemmArgs {
+    int n_rows, row0, dim, ld, kp, np, comp;
+    ObjDesc O;
+    const double* pos0;  // SEL (sel != nullptr): candidate of slot r in its alternate buffer
+    const double* pos1;
+    const uint8_t* sel;
+    uint8_t* sel_next;
+    const double* pos;  // dense: old rows (through order if non-null)
+    double* out_pos;    // dense: candidates in, kept rows out
+    const int* order;
+    uint8_t* out_acc;
+    uint8_t* out_warn;
+    const double* fit;
+    double* out_fit;
+    const uint8_t* cand_ok;
+    unsigned long long* warn_count;
+    unsigned long long* trace_key;
+    double* Y;  // scratch (set by cec_gemm_finish)
+    double* Z;
+};
+int cec_gemm_finish(const CecGemmArgs& A, cudaStream_t st, int num_sms);
+__host__ __device__ inline int gemm_kp(int dim) { return (dim + 15) & ~15; }
+__host__ __device__ inline int gemm_np(int dim) { return (dim + 63) & ~63; }
 
 // Kernel getters (defined in the instantiating TUs).
 const void* pick_update_sel(int dim, bool cand_only, bool cec);

@@ -162,10 +162,13 @@ struct UpdateResult {
 
 // One protozoon, one warp.  `out_row` receives the kept row.  All lanes of
 // the warp must call this with identical arguments.
+// cand_only: write the clamped candidate to out_row and return its finiteness
+// in `accepted` (the fitness, greedy select and best-so-far run later: the
+// CEC2022 large-D GEMM path, apo_gemm.cuh).
 template <class Rows>
 __device__ inline UpdateResult update_protozoon(const IterParams& P, const ObjDesc& O, const Rows& R, int i,
                                                 bool in_dr, double p_dr_i, double* out_row, const WarpScratch& s,
-                                                int lane) {
+                                                int lane, bool cand_only = false) {
     const int ps = P.ps, dim = P.dim;
     const double* x = R.row(i);
     const double fit_i = R.fitness(i);
@@ -298,6 +301,12 @@ __device__ inline UpdateResult update_protozoon(const IterParams& P, const ObjDe
     res.accepted = false;
     res.warned = false;
     res.fitness = fit_i;
+    if (cand_only) {
+        for (int d = lane; d < dim; d += 32) out_row[d] = s.cand[d];
+        res.accepted = ok;
+        __syncwarp();
+        return res;
+    }
     if (ok) {
         const double nf = eval_warp(O, s.cand, s.terms, dim, lane, s.aux);
         if (isfinite(nf)) {

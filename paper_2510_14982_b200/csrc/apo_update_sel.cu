@@ -12,7 +12,8 @@ const void* pick_update_sel(int dim, bool cand_only, bool cec) {
         if (dim <= 32) return (const void*)k_update_group<true, 1, KIND_CAND>;
         if (dim <= 64) return (const void*)k_update_group<true, 2, KIND_CAND>;
         if (dim <= 128) return (const void*)k_update_group<true, 4, KIND_CAND>;
-        return nullptr;
+        if (dim <= kGroupMaxDim) return (const void*)k_update_group<true, 0, KIND_CAND>;
+        return (const void*)k_update<true>;  // candidates-only through UpdArgs::cand_ok
     }
     if (dim > kGroupMaxDim) return (const void*)k_update<true>;
     if (cec) return (const void*)k_update_group<true, 0, KIND_ANY>;

@@ -182,6 +182,15 @@ class DeviceObjective:
                     pad[0, :dim, :dim] = rot_t[0][:, np.asarray(shuffle) - 1]
                 arrays.append(("rot_pad", pad))
                 table = elliptic_weights(dim)  # ELLIPS weights 10^(6i/(D-1)), host libm like the oracle
+            elif getattr(obj.data, "rotation", "dmma") == "dmma" and obj.code - 100 in (1, 2, 3, 4, 5, 6, 7, 8, 10):
+                # D > 104: the rotated component's M^T padded for the DMMA GEMM (apo_cec_gemm.cu)
+                comp = 1 if obj.code - 100 == 10 else 0
+                kp, np_ = (dim + 15) // 16 * 16, (dim + 63) // 64 * 64
+                gm = np.zeros((kp, np_))
+                gm[:dim, :dim] = rot_t[comp]
+                if obj.code - 100 in (6, 7, 8):
+                    gm[:dim, :dim] = rot_t[0][:, np.asarray(shuffle) - 1]
+                arrays.append(("rot_gemm", gm))
             for field, arr in arrays:
                 t = torch.as_tensor(np.array(arr), device=dev)
                 self.keep.append(t)

@@ -79,7 +79,7 @@ def test_teacher_forced_step_matches_oracle(fn):
     from paper_2510_14982_b200.kernels import get_backend
 
     name = f"cec2022_f{fn}"
-    for ps, dim in ((100, 20), (3000, 50), (2000, 100), (300, 12)):
+    for ps, dim in ((100, 20), (3000, 50), (2000, 100), (300, 12), (700, 150), (260, 300)):
         cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=50, seed=fn)
         pos, fit = oracle.initialize(fn, ps, dim, -100.0, 100.0, name)
         order = oracle.argsort_stable(fit)
@@ -138,3 +138,25 @@ def test_fma_rotation_path_matches_oracle(fn):
         agree = got[2] == want[2]
         assert agree.mean() > 0.99, rot
         np.testing.assert_allclose(got[1][agree], want[1][agree], rtol=RTOL)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fn", [1, 6, 10])
+def test_large_dim_gemm_device_loop_matches_dense_path(fn):
+    """D > 104: the device loop (slot layout, per-slot buffer selectors) through the DMMA GEMM path
+    equals the dense reference-facing path step for step."""
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200 import engine
+
+    name = f"cec2022_f{fn}"
+    cfg = pz.ApoConfig(ps=500, dim=300, bounds=pz.Bounds(-100.0, 100.0, 300), max_iterations=6, seed=fn)
+    run = engine.DeviceRun(cfg, pz.get_objective(name))
+    run.initialize()
+    run.iterate(6)
+    pos, fit = run.population()
+    run.close()
+    pop = pz.initialize(cfg, name)
+    for t in range(6):
+        pop = pz.step(pop, cfg, name, t)
+    np.testing.assert_allclose(fit, pop.fitness, rtol=1e-12)
+    np.testing.assert_allclose(pos, pop.positions, rtol=1e-12)
