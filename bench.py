@@ -67,7 +67,13 @@ def dist_setup(backend):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend=backend)
+        if backend == "nccl":
+            import torch
+
+            torch.cuda.set_device(local)  # bind this rank's GPU before NCCL creates its communicator
+            dist.init_process_group(backend=backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend=backend)
     return rank, world, local
 
 
@@ -317,6 +323,7 @@ def bench_ours(args, rank, world, local):
             result["c4_sharded"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if not args.no_e2e:
         result["e2e"] = bench_e2e(m["cfg"], m["obj"], K, rank, world)
+        result["e2e_run"] = bench_e2e_run(m["cfg"], m["obj"], rank, world)
     if not args.no_suite and rank == 0:
         result["suite_c2"] = bench_suite(world)
         result["suite_c3"] = bench_c3()
@@ -377,6 +384,27 @@ def bench_e2e(cfg, obj, K, rank, world):
     nb = 8 * cfg.ps * cfg.dim + 8 * cfg.ps
     return {"value": world * cfg.ps * n / dt, "unit": UNIT, "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
             "steps": n, "api": "paper_2510_14982_b200.step(Population numpy) -> Population numpy"}
+
+
+def bench_e2e_run(cfg, obj, rank, world, T=30):
+    """A whole engine.run (the loop resident on the device) end to end: initialisation, T iterations,
+    and the RunResult on the host (trace, best, final population D2H) -- evals/s over ps * T."""
+    import dataclasses
+
+    import torch
+
+    import paper_2510_14982_b200 as pz
+
+    c = dataclasses.replace(cfg, max_iterations=T)
+    pz.run(dataclasses.replace(c, max_iterations=3), obj)  # warm-up (allocations, page-locked buffers)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    res = pz.run(c, obj)
+    dt = max_over_ranks(time.perf_counter() - t0, world)
+    return {"value": world * c.ps * T / dt, "unit": UNIT, "iterations": T, "seconds": dt,
+            "d2h_bytes": int(res.population.positions.nbytes + res.population.fitness.nbytes + res.trace.nbytes),
+            "api": "paper_2510_14982_b200.run(cfg, objective) -> RunResult (host arrays)"}
 
 
 def bench_suite(world):
@@ -472,7 +500,7 @@ def bench_c5(sizes=(10, 20, 50, 100, 1000), fns=(1, 4, 10), ps=10_000, iters=20,
     rows = []
     for fn in fns:
         for dim in sizes:
-            for rot in (("dmma", "fma") if dim <= 104 else ("fma",)):
+            for rot in ("dmma", "fma"):
                 obj = pz.cec2022_objective(fn, rotation=rot)
                 cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=iters + 3)
                 run = DeviceRun(cfg, obj)
@@ -601,6 +629,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
+        dist.barrier()  # rank 0 may still be running the single-GPU suites
         dist.destroy_process_group()
 
 
