@@ -595,9 +595,7 @@ def bench_reference(args, rank, world):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k_run, "warmup": W,
         "ms_per_step": dt * 1e3 / k_run, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"C4: single population ps={ps} D={dim} objective={args.objective}"
-                               + (" (stand-in for CEC2022 F6/F10)" if args.objective in pz.FUNCTION_NAMES else ""),
-                   "ps": ps, "dim": dim, "iterations_per_step": 1},
+        "config": {"workload": c4_workload(args.objective, ps, dim), "ps": ps, "dim": dim, "iterations_per_step": 1},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port", "sample": sample,
                          "cpu": _cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
