@@ -156,6 +156,12 @@ int apo_run_create(apo_run **out, int64_t ps, int64_t dim, int64_t max_iteration
                    double pf_max, double lower, double upper, double eps, const apo_objective *objective_host,
                    const double *sched_host, const double *p_dr_host, int rng, void *stream);
 int apo_run_initialize(apo_run *run);
+/* Checkpoint/resume: load a population (reference row order, [ps][dim]) that
+ * has completed `iteration` iterations; the next apo_run_iterate continues the
+ * run exactly (every draw is keyed by (seed, iteration, rank, slot)).  Trace
+ * entries before `iteration` are not kept. */
+int apo_run_load(apo_run *run, const double *positions, const double *fitness, int is_host, int64_t iteration,
+                 int64_t warnings);
 /* Runs iterations [t, t+n) where t is the number already run. */
 int apo_run_iterate(apo_run *run, int64_t n);
 /* Trace entries 0..iterations_run as doubles (host buffer of >= n+1). */

@@ -124,6 +124,7 @@ PROTOTYPES = {
                               _P, _P, _INT, _P]),
     "apo_run_initialize": (_INT, [_P]),
     "apo_run_iterate": (_INT, [_P, _I]),
+    "apo_run_load": (_INT, [_P, _P, _P, _INT, _I, _I]),
     "apo_run_trace": (_INT, [_P, _P, _I]),
     "apo_run_population": (_INT, [_P, _P, _P, _INT]),
     "apo_run_best": (_INT, [_P, _P, _P, C.POINTER(C.c_int64)]),

@@ -891,6 +891,30 @@ int apo_run_iterate(apo_run* r, int64_t n) {
     return APO_OK;
 }
 
+int apo_run_load(apo_run* r, const double* positions, const double* fitness, int is_host, int64_t iteration,
+                 int64_t warnings) {
+    APO_CHECK(r && positions && fitness, "NULL argument");
+    APO_CHECK(iteration >= 0 && iteration <= r->T, "iteration outside [0, max_iterations]");
+    cudaStream_t st = r->stream;
+    const cudaMemcpyKind kind = is_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    // rows in reference row order become slots 0..ps-1 (identity order, buffer 0): exactly the state
+    // the device loop would hold, since the next stable sort breaks ties by that order
+    APO_CUDA(cudaMemcpy2DAsync(r->pos[0], 8 * (size_t)r->ld, positions, 8 * (size_t)r->dim, 8 * (size_t)r->dim,
+                               (size_t)r->ps, kind, st));
+    APO_CUDA(cudaMemcpyAsync(r->fit[0], fitness, 8 * (size_t)r->ps, kind, st));
+    APO_CUDA(cudaMemsetAsync(r->sel[0], 0, (size_t)r->ps, st));
+    k_iota<<<grid_for(r->ps, 256), 256, 0, st>>>((int)r->ps, r->order);
+    APO_CUDA(cudaGetLastError());
+    APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(r->T + 1), st));
+    const unsigned long long w = (unsigned long long)warnings;
+    APO_CUDA(cudaMemcpyAsync(r->warn, &w, 8, cudaMemcpyHostToDevice, st));
+    APO_CUDA(cudaStreamSynchronize(st));  // w lives on this stack frame
+    r->cur = 0;
+    r->iters = iteration;
+    r->initialized = true;
+    return APO_OK;
+}
+
 int apo_run_trace(apo_run* r, double* trace_host, int64_t n) {
     APO_CHECK(r && trace_host && n >= 0 && n <= r->T, "bad arguments");
     std::vector<unsigned long long> k((size_t)n + 1);

@@ -213,6 +213,16 @@ class DeviceRun:
     def initialize(self):
         _lib.check(self.lib.apo_run_initialize(self.handle), "apo_run_initialize")
 
+    def load(self, pop: Population):
+        """Resume from a checkpointed population (reference row order) after pop.iteration iterations."""
+        pos = np.ascontiguousarray(pop.positions, dtype=np.float64)
+        fit = np.ascontiguousarray(pop.fitness, dtype=np.float64)
+        if pos.shape != (self.cfg.ps, self.cfg.dim) or fit.shape != (self.cfg.ps,):
+            raise ValueError("population shape does not match the run configuration")
+        _lib.check(self.lib.apo_run_load(self.handle, pos.ctypes.data, fit.ctypes.data, 1, int(pop.iteration),
+                                         int(pop.warnings)), "apo_run_load")
+        self.start_iteration = int(pop.iteration)
+
     def iterate(self, n: int):
         _lib.check(self.lib.apo_run_iterate(self.handle, n), "apo_run_iterate")
 
@@ -317,6 +327,38 @@ def run(cfg: ApoConfig, objective, mode: Optional[EngineMode] = None, backend: O
     return RunResult(best_position=best_x, best_fitness=best_f, trace=trace, iterations_run=it, fe_count=fe,
                      warnings=warned, wall_clock_seconds=seconds, mode=mode.kind, workers=workers, backend=bk.NAME,
                      config_echo=cfg,
+                     population=Population(pos, fit, iteration=it, fe_count=fe, warnings=warned))
+
+
+def resume(cfg: ApoConfig, objective, population: Population, backend: Optional[str] = None) -> RunResult:
+    """Continue a run from a checkpointed Population (e.g. RunResult.population or a step() result) up to
+    cfg's iteration / evaluation budget, on the device-resident loop.  Exact: the continuation equals the
+    uninterrupted run (every draw is keyed by seed, iteration, individual and slot -- rng.py:1-19).
+    The reference has no checkpointing; this is SURVEY.md 8(f) item 4."""
+    obj = resolve_objective(objective)
+    bk = _resolve_backend(obj, backend)
+    _check(cfg, obj)
+    if population.size != cfg.ps or population.dim != cfg.dim:
+        raise ValueError("population shape does not match the configuration")
+    n_total = cfg.iterations_within_budget()
+    start = int(population.iteration)
+    if not 0 <= start <= n_total:
+        raise ValueError(f"population.iteration {start} outside [0, {n_total}]")
+    started = time.perf_counter()
+    dr = DeviceRun(cfg, obj)
+    try:
+        dr.load(population)
+        dr.iterate(n_total - start)
+        it, fe, warned = dr.counters()
+        trace = dr.trace(it)[start:]
+        trace[0] = float(np.min(population.fitness))
+        best_f, best_x, _ = dr.best()
+        pos, fit = dr.population()
+    finally:
+        dr.close()
+    return RunResult(best_position=best_x, best_fitness=best_f, trace=trace, iterations_run=it, fe_count=fe,
+                     warnings=warned, wall_clock_seconds=time.perf_counter() - started, mode=SEQUENTIAL, workers=1,
+                     backend=bk.NAME, config_echo=cfg,
                      population=Population(pos, fit, iteration=it, fe_count=fe, warnings=warned))
 
 
