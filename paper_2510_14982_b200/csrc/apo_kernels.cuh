@@ -515,6 +515,9 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         if (lane == 0) v = atomicAdd(A.tile_counter, 1u);
         return (int)__shfl_sync(kFull, v, 0);
     };
+    // split form: the atomic is issued at the top of a tile and its value consumed at the bottom
+    auto claim_issue = [&]() -> unsigned { return lane == 0 ? atomicAdd(A.tile_counter, 1u) : 0u; };
+    auto claim_take = [&](unsigned v) -> int { return (int)__shfl_sync(kFull, v, 0); };
     (void)stride;
     int tile = claim();
     int tile_nxt = 0;
@@ -551,12 +554,12 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         } else {
             issue(tile, 0, cur);
             cp_async_commit();
-            tile_next = tile_nxt;  // claimed one tile ahead: the atomic's latency hides behind this tile
-            tile_nxt = tile_next < ntiles ? claim() : ntiles;
+            tile_next = tile_nxt;  // claimed one tile ahead
             sel_cur = sel_nxt;
-            sel_nxt = sel_of(tile_nxt);
             cp_async_wait_all();
         }
+        // the claim after next: issued now, read after the evaluation (its latency hides behind it)
+        const unsigned pending = (!pf && tile_next < ntiles) ? claim_issue() : 0u;
         __syncwarp();
         const double* qsrc = nullptr;  // this quad's candidate row (compositions re-read it per component)
         if (live) qsrc = SEL ? (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
@@ -595,6 +598,10 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         }
         __syncwarp();
         if (pf) buf ^= 1;
+        if (!pf) {
+            tile_nxt = tile_next < ntiles ? claim_take(pending) : ntiles;
+            sel_nxt = sel_of(tile_nxt);
+        }
         tile = tile_next;
     }
     cp_async_wait_all();
