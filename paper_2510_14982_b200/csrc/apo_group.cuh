@@ -54,7 +54,10 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // Row staging ring: kStages protozoa x 4 rows, per warp (HBM-resident paths).
-constexpr int kStages = 2;
+#ifndef APO_STAGES
+#define APO_STAGES 2
+#endif
+constexpr int kStages = APO_STAGES;
 #ifndef APO_STAGE_MAX_DIM
 #define APO_STAGE_MAX_DIM 128
 #endif
