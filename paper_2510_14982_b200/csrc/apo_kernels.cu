@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(kThreads) k_init(int rng, uint64_t seed, int p
             row[d] = c;
         }
         __syncwarp();
+        if (!fit) continue;  // positions only (k_cec_eval evaluates them)
         const double f = eval_warp(O, s.cand, s.terms, dim, lane, s.aux);
         if (lane == 0) fit[r0] = f;
         const unsigned long long k = sort_key(f);
@@ -301,6 +302,9 @@ int smem_optin() {
 // k_cec_eval evaluates them in DMMA tiles and finishes the update.
 // mid_event (nullable) is recorded between the two.
 
+int launch_cec_eval(bool sel_mode, const UpdArgs& a, cudaStream_t st, uint8_t* cand_ok, unsigned* tile_counter,
+                    int init);
+
 int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* cand_ok = nullptr,
                   cudaEvent_t mid_event = nullptr, unsigned* tile_counter = nullptr) {
     UpdArgs a = A0;
@@ -366,7 +370,17 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         return APO_OK;
     }
     if (!split) return APO_OK;
+    return launch_cec_eval(sel_mode, a, st, cand_ok, tile_counter, 0);
+}
+
+// k_cec_eval over ranks [rank_lo, rank_hi) of an update (init = 0) or over every slot of pos0 at
+// iteration 0 (init = 1).
+int launch_cec_eval(bool sel_mode, const UpdArgs& a, cudaStream_t st, uint8_t* cand_ok, unsigned* tile_counter,
+                    int init) {
+    const int dim = a.P.dim;
+    const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
     CecEvalArgs E{};
+    E.init = init;
     E.row0 = a.rank_lo;
     E.n_rows = a.rank_hi - a.rank_lo;
     E.order = sel_mode ? nullptr : a.order;
@@ -635,9 +649,29 @@ int apo_initialize(uint64_t seed, int64_t ps, int64_t dim, int64_t ld, double lo
     if (int rc = set_smem((const void*)k_init, smem)) return rc;
     const long long need = (ps + w - 1) / w;
     const long long cap = 8LL * num_sms();
+    const ObjDesc O = to_desc(objective_host);
+    // CEC2022 with DMMA tables: the same evaluator as the device loop's iteration 0 (k_cec_eval, init mode)
+    const bool cec_fast = O.code > APO_OBJ_CEC2022_BASE && dim <= kCecEvalMaxDim && O.cec.rot_pad;
     k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, as_stream(stream)>>>(
-        RNG_KEYED, seed, (int)ps, (int)dim, (int)ld, lower, span, to_desc(objective_host), positions, fitness, nullptr);
+        RNG_KEYED, seed, (int)ps, (int)dim, (int)ld, lower, span, O, positions, cec_fast ? nullptr : fitness, nullptr);
     APO_CUDA(cudaGetLastError());
+    if (cec_fast) {
+        unsigned* counter = nullptr;
+        APO_CUDA(cudaMallocAsync((void**)&counter, 16, as_stream(stream)));
+        UpdArgs A{};
+        A.P.ps = (int)ps;
+        A.P.dim = (int)dim;
+        A.P.ld = (int)ld;
+        A.O = O;
+        A.pos0 = positions;
+        A.pos1 = positions;
+        A.out_fit = fitness;
+        A.rank_lo = 0;
+        A.rank_hi = (int)ps;
+        const int rc = launch_cec_eval(true, A, as_stream(stream), nullptr, counter, 1);
+        cudaFreeAsync(counter, as_stream(stream));
+        if (rc) return rc;
+    }
     return APO_OK;
 }
 
@@ -812,10 +846,26 @@ int apo_run_initialize(apo_run* r) {
     const long long cap = (long long)(per_sm > 0 ? per_sm : 1) * num_sms();
     APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(r->T + 1), st));
     APO_CUDA(cudaMemsetAsync(r->warn, 0, 8, st));
+    // CEC2022 with DMMA tables: k_init draws the rows, k_cec_eval (init mode) evaluates them
+    const bool cec_fast = r->obj.code > APO_OBJ_CEC2022_BASE && r->dim <= kCecEvalMaxDim && r->obj.cec.rot_pad;
     k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, st>>>(r->rng, r->seed, (int)r->ps, (int)r->dim, (int)r->ld,
                                                                   r->lower, r->upper - r->lower, r->obj, r->pos[0],
-                                                                  r->fit[0], r->trace_keys);
+                                                                  cec_fast ? nullptr : r->fit[0], r->trace_keys);
     APO_CUDA(cudaGetLastError());
+    if (cec_fast) {
+        UpdArgs A{};
+        A.P.ps = (int)r->ps;
+        A.P.dim = (int)r->dim;
+        A.P.ld = (int)r->ld;
+        A.O = r->obj;
+        A.pos0 = r->pos[0];
+        A.pos1 = r->pos[0];
+        A.out_fit = r->fit[0];
+        A.trace_key = r->trace_keys;
+        A.rank_lo = 0;
+        A.rank_hi = (int)r->ps;
+        if (int rc = launch_cec_eval(true, A, st, r->cand_ok, r->tile_counter, 1)) return rc;
+    }
     k_iota<<<grid_for(r->ps, 256), 256, 0, st>>>((int)r->ps, r->order);
     APO_CUDA(cudaGetLastError());
     APO_CUDA(cudaMemsetAsync(r->sel[0], 0, (size_t)r->ps, st));
@@ -1144,11 +1194,27 @@ int apo_shard_initialize(apo_shard* r) {
     const long long cap = 8LL * num_sms();
     APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(r->T + 1), st));
     APO_CUDA(cudaMemsetAsync(r->warn, 0, 8, st));
-    // every process builds the identical iteration-0 population (replicated, no exchange)
+    // every process builds the identical iteration-0 population (replicated, no exchange), with the
+    // same evaluator as the single-GPU device loop (k_cec_eval in init mode for CEC2022)
+    const bool cec_fast = r->obj.code > APO_OBJ_CEC2022_BASE && r->dim <= kCecEvalMaxDim && r->obj.cec.rot_pad;
     k_init<<<(int)(need < cap ? need : cap), 32 * w, smem, st>>>(r->rng, r->seed, (int)r->ps, (int)r->dim, (int)r->ld,
                                                                   r->lower, r->upper - r->lower, r->obj, r->pos[0],
-                                                                  r->fit[0], r->trace_keys);
+                                                                  cec_fast ? nullptr : r->fit[0], r->trace_keys);
     APO_CUDA(cudaGetLastError());
+    if (cec_fast) {
+        UpdArgs A{};
+        A.P.ps = (int)r->ps;
+        A.P.dim = (int)r->dim;
+        A.P.ld = (int)r->ld;
+        A.O = r->obj;
+        A.pos0 = r->pos[0];
+        A.pos1 = r->pos[0];
+        A.out_fit = r->fit[0];
+        A.trace_key = r->trace_keys;
+        A.rank_lo = 0;
+        A.rank_hi = (int)r->ps;
+        if (int rc = launch_cec_eval(true, A, st, nullptr, r->tile_counter, 1)) return rc;
+    }
     r->cur = 0;
     r->iters = 0;
     return APO_OK;

@@ -437,6 +437,7 @@ struct CecEvalArgs {
     int prefetch;            // FAST: double-buffer X with cp.async (else one X tile per warp, more warps)
     int bsm_comp;            // FAST: the component whose rotation is staged in shared memory
     int ncomp;               // shift vectors to stage
+    int init;                // iteration 0: evaluate the rows of pos0 (slot order) into out_fit, no select
 };
 
 // FAST (F1-F8: one rotation): the CTA stages that rotation in shared memory
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         const double* src = nullptr;
         if (live) {
             const int r = row_of(tile);
-            if constexpr (SEL) src = (selq ? A.pos0 : A.pos1) + (size_t)r * A.ld;  // the slot's alternate buffer
+            if constexpr (SEL) src = (selq || A.init ? A.pos0 : A.pos1) + (size_t)r * A.ld;  // the alternate buffer
             else src = A.out_pos + (size_t)r * A.ld;
         }
         for (int i = t; i < n4; i += 4) {
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         }
     };
     auto sel_of = [&](int tile) -> uint8_t {
-        if constexpr (SEL) return live_in(tile) ? A.sel[row_of(tile)] : (uint8_t)0;
+        if constexpr (SEL) return (live_in(tile) && !A.init) ? A.sel[row_of(tile)] : (uint8_t)0;
         return 0;
     };
     // dynamic tile claims (lane 0 + broadcast) keep the warps of an SM finishing together
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         // per-row scalars for the select, loaded early so their latency hides behind the evaluation
         bool ok = false;
         double fit_i = 0.0;
-        if (live && t == 0) {
+        if (live && t == 0 && !A.init) {
             ok = A.cand_ok[r] != 0;
             fit_i = A.fit[(!SEL && A.order) ? A.order[r] : r];
         }
@@ -562,10 +563,16 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         const unsigned pending = (!pf && tile_next < ntiles) ? claim_issue() : 0u;
         __syncwarp();
         const double* qsrc = nullptr;  // this quad's candidate row (compositions re-read it per component)
-        if (live) qsrc = SEL ? (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
+        if (live) qsrc = SEL ? (cur || A.init ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
         const double nf = cec_eval_quad<NT>(C, Xb[buf], qsrc, cs, dim, lane, ew, bsm, A.bsm_comp);
         bool acc = false;
-        if (live && t == 0) {
+        if (A.init) {  // iteration 0 (engine.py:116-139): the fitness of every initial row
+            if (live && t == 0) {
+                A.out_fit[r] = nf;
+                const unsigned long long k = sort_key(nf);
+                my_min = k < my_min ? k : my_min;
+            }
+        } else if (live && t == 0) {
             double kept = fit_i;
             bool warned = false;
             if (ok && isfinite(nf)) {

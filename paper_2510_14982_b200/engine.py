@@ -244,6 +244,7 @@ class DeviceRun:
         return f.value, x, row.value
 
     def population(self):
+        """(positions, fitness) in reference row order, host numpy arrays."""
         pos = np.empty((self.cfg.ps, self.cfg.dim))
         fit = np.empty(self.cfg.ps)
         _lib.check(self.lib.apo_run_population(self.handle, pos.ctypes.data, fit.ctypes.data, 1),
