@@ -11,7 +11,8 @@ from paper_2510_14982_b200.engine import DeviceRun
 name = sys.argv[1] if len(sys.argv) > 1 else "cec2022_f6"
 dim = int(sys.argv[2]) if len(sys.argv) > 2 else 100
 ps = int(sys.argv[3]) if len(sys.argv) > 3 else 1_000_000
-cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=100, seed=0)
+rng = sys.argv[4] if len(sys.argv) > 4 else "keyed"
+cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=100, seed=0, rng=rng)
 run = DeviceRun(cfg, pz.get_objective(name))
 run.initialize()
 run.iterate(3)
@@ -19,4 +20,4 @@ torch.cuda.synchronize()
 run.profile(True)
 run.iterate(5)
 a, b, n = run.profile_split()
-print(f"{name} D={dim} ps={ps}: candidates {a / n:.3f} ms  evaluate {b / n:.3f} ms  per iteration")
+print(f"{name} D={dim} ps={ps} rng={rng}: candidates {a / n:.3f} ms  evaluate {b / n:.3f} ms  per iteration")
