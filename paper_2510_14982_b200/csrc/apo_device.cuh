@@ -116,8 +116,11 @@ __host__ __device__ __forceinline__ Key stream_key(int mode, uint64_t seed, uint
     return k;
 }
 
+#ifndef APO_PHILOX_INLINE
+#define APO_PHILOX_INLINE __noinline__
+#endif
 #ifdef __CUDA_ARCH__
-__device__ __noinline__ double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
+__device__ APO_PHILOX_INLINE double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
     return (double)(philox4x32_10((uint32_t)counter, (uint32_t)(counter >> 32), b, c, (uint32_t)seed,
                                   (uint32_t)(seed >> 32)) >> 11) * kInv2p53;
 }
