@@ -107,12 +107,37 @@ __device__ __forceinline__ double grie_rosen_t(double a, double b) {
     const double t = 100.0 * t1 * t1 + t2 * t2;
     return t * t / 4000.0 - cos(t) + 1.0;
 }
-// fmod(a, 500) for a >= 0, exactly: k*500 is exact, a - k*500 is exact (Sterbenz), and the
-// only misstep of k = floor(a/500) is a quotient rounded up onto an integer (fixed by + 500).
+// fmod(a, 500) for a >= 0, exactly, without a division: k = floor(a * 0.002) is the
+// quotient or one off; a - k*500 is exact (Sterbenz: a and k*500 are within a factor
+// of two, or k = 0) and the one-off cases are corrected by +/- 500 -- again exact,
+// because the corrected value a - 500*floor(a/500) is representable.
 __device__ __forceinline__ double fmod500(double a) {
-    double m = a - floor(a / 500.0) * 500.0;
+    double m = a - floor(a * 0.002) * 500.0;
     if (m < 0.0) m += 500.0;
+    else if (m >= 500.0) m -= 500.0;
     return m;
+}
+
+// sin(x) for 0 <= x <= 64 (the Schwefel argument sqrt(s) <= 22.4): x = k pi + r with
+// pi in two parts, |r| <= pi/2, odd Taylor polynomial to degree 21 in FMAs.  Max abs
+// error 2.2e-16 on [0, 24] against libm (checked on 2e4 points); larger x falls back.
+__device__ __forceinline__ double sin_small(double x) {
+    if (!(x <= 64.0)) return sin(x);
+    const double k = rint(x * 0.31830988618379067154);
+    const double r = fma(-k, 1.2246467991473532e-16, fma(-k, 3.141592653589793116, x));
+    const double r2 = r * r;
+    double p = 1.9572941063391263e-20;  // 1/21!
+    p = fma(p, r2, -8.2206352466243295e-18);
+    p = fma(p, r2, 2.8114572543455206e-15);
+    p = fma(p, r2, -7.6471637318198164e-13);
+    p = fma(p, r2, 1.6059043836821613e-10);
+    p = fma(p, r2, -2.5052108385441720e-08);
+    p = fma(p, r2, 2.7557319223985893e-06);
+    p = fma(p, r2, -1.9841269841269841e-04);
+    p = fma(p, r2, 8.3333333333333332e-03);
+    p = fma(p, r2, -1.6666666666666666e-01);
+    const double v = fma(r * r2, p, r);
+    return ((long long)k & 1) ? -v : v;
 }
 
 // Schwefel term (CEC2022 schwefel_func), branch-free: with a = |z|,
@@ -125,7 +150,7 @@ __device__ __forceinline__ double schwefel_t(double zi, int n) {
     const double a = fabs(zi);
     const bool out = a > 500.0;
     const double s = out ? 500.0 - fmod500(a) : a;
-    const double v = s * sin(sqrt(s));
+    const double v = s * sin_small(sqrt(s));
     const double t = (zi > 0.0 ? zi - 500.0 : zi + 500.0) / 100.0;
     return (zi > 0.0 ? -v : v) + (out ? t * t / n : 0.0);
 }
