@@ -427,14 +427,18 @@ def bench_suite(world):
     pz.run_batch(cfg, names[:24], seeds[:24], want_trace=False, device_out=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    res = pz.run_batch(cfg, names, seeds, want_trace=False, device_out=True)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    times = []
+    for _ in range(3):  # the launch's time is its slowest SM's three co-resident runs: report the median
+        e0.record()
+        res = pz.run_batch(cfg, names, seeds, want_trace=False, device_out=True)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
     evals = len(names) * cfg.ps * cfg.max_iterations
     best = res.best_fitness.cpu().numpy().reshape(12, 30)
-    return {"value": evals / (ms / 1e3), "unit": UNIT, "ms": ms, "runs": len(names),
+    return {"value": evals / (ms / 1e3), "unit": UNIT, "ms": ms, "ms_all": [round(t, 1) for t in times],
+            "runs": len(names),
             "workload": "C2: CEC2022 F1-F12 (synthetic data) x 30 seeds, D=20, ps=100, T=1000, one CTA per run",
             "median_best_minus_fstar": [float(np.median(best[k]) - pz.cec2022.FSTAR[k]) for k in range(12)],
             "gpus": 1}

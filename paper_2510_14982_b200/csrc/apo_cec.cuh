@@ -613,58 +613,61 @@ __device__ __forceinline__ void cec_rotate_quad(const double* __restrict__ rot_p
 
 // Basic function b over z[0..n) by the 4 lanes of a quad; every lane of the
 // quad returns the value.  ew: host-computed ELLIPS weights (nullable).
-__device__ inline double cec_basic_quad(int b, const double* z, int n, int t, const double* ew) {
+// Z(i): element i of the basic function's input (a stored row, or an affine map of the candidate
+// computed on the fly -- unrotated composition components need no scratch pass).
+template <class Zf>
+__device__ inline double cec_basic_quad_t(int b, const Zf& Z, int n, int t, const double* ew) {
     double a = 0.0, c = 0.0;
     switch (b) {
     case B_ZAKHAROV:
         for (int i = t; i < n; i += 4) {
-            a += z[i] * z[i];
-            c += 0.5 * (i + 1) * z[i];
+            a += Z(i) * Z(i);
+            c += 0.5 * (i + 1) * Z(i);
         }
         a = qsum(a);
         c = qsum(c);
         return a + c * c + c * c * c * c;
     case B_ROSENBROCK:
         for (int i = t; i < n - 1; i += 4) {
-            const double t1 = z[i] * z[i] - z[i + 1], t2 = z[i] - 1.0;
+            const double t1 = Z(i) * Z(i) - Z(i + 1), t2 = Z(i) - 1.0;
             a += 100.0 * t1 * t1 + t2 * t2;
         }
         return qsum(a);
     case B_ESCAFFER6:
-        for (int i = t; i < n; i += 4) a += schaffer_g(z[i], z[i + 1 < n ? i + 1 : 0]);
+        for (int i = t; i < n; i += 4) a += schaffer_g(Z(i), Z(i + 1 < n ? i + 1 : 0));
         return qsum(a);
     case B_RASTRIGIN:
     case B_STEP_RASTRIGIN:
-        for (int i = t; i < n; i += 4) a += z[i] * z[i] - 10.0 * cospi(2.0 * z[i]) + 10.0;
+        for (int i = t; i < n; i += 4) a += Z(i) * Z(i) - 10.0 * cospi(2.0 * Z(i)) + 10.0;
         return qsum(a);
     case B_LEVY: {
         for (int i = t; i < n - 1; i += 4) {
-            const double wi = 1.0 + z[i] / 4.0;
+            const double wi = 1.0 + Z(i) / 4.0;
             const double s = sin(kPi * wi + 1.0);
             a += (wi - 1.0) * (wi - 1.0) * (1.0 + 10.0 * s * s);
         }
         a = qsum(a);
-        const double w0 = 1.0 + z[0] / 4.0, wn = 1.0 + z[n - 1] / 4.0;
+        const double w0 = 1.0 + Z(0) / 4.0, wn = 1.0 + Z(n - 1) / 4.0;
         const double s0 = sin(kPi * w0), sn = sin(2.0 * kPi * wn);
         return s0 * s0 + a + (wn - 1.0) * (wn - 1.0) * (1.0 + sn * sn);
     }
     case B_BENT_CIGAR:
         for (int i = t; i < n; i += 4)
-            if (i >= 1) a += z[i] * z[i];
-        return z[0] * z[0] + 1e6 * qsum(a);
+            if (i >= 1) a += Z(i) * Z(i);
+        return Z(0) * Z(0) + 1e6 * qsum(a);
     case B_DISCUS:
         for (int i = t; i < n; i += 4)
-            if (i >= 1) a += z[i] * z[i];
-        return 1e6 * z[0] * z[0] + qsum(a);
+            if (i >= 1) a += Z(i) * Z(i);
+        return 1e6 * Z(0) * Z(0) + qsum(a);
     case B_ELLIPS:
         for (int i = t; i < n; i += 4)
-            a += (ew ? ew[i] : pow(10.0, 6.0 * i / (n > 1 ? n - 1 : 1))) * z[i] * z[i];
+            a += (ew ? ew[i] : pow(10.0, 6.0 * i / (n > 1 ? n - 1 : 1))) * Z(i) * Z(i);
         return qsum(a);
     case B_HGBAT:
     case B_HAPPYCAT: {
         for (int i = t; i < n; i += 4) {
-            a += z[i] * z[i];
-            c += z[i];
+            a += Z(i) * Z(i);
+            c += Z(i);
         }
         a = qsum(a);
         c = qsum(c);
@@ -681,7 +684,7 @@ __device__ inline double cec_basic_quad(int b, const double* z, int n, int t, co
             for (int j = 1; j <= 32; j++) {
                 t1 *= 2.0;  // 2^j and 2^-j are exact
                 inv *= 0.5;
-                const double t2 = t1 * z[i];
+                const double t2 = t1 * Z(i);
                 s += fabs(t2 - floor(t2 + 0.5)) * inv;
             }
             pr *= pow(1.0 + (i + 1) * s, 10.0 / t3);
@@ -692,19 +695,19 @@ __device__ inline double cec_basic_quad(int b, const double* z, int n, int t, co
     }
     case B_ACKLEY: {
         for (int i = t; i < n; i += 4) {
-            a += z[i] * z[i];
-            c += cospi(2.0 * z[i]);
+            a += Z(i) * Z(i);
+            c += cospi(2.0 * Z(i));
         }
         a = qsum(a);
         c = qsum(c);
         return kE - 20.0 * exp(-0.2 * sqrt(a / n)) - exp(c / n) + 20.0;
     }
     case B_SCHWEFEL:
-        for (int i = t; i < n; i += 4) a += schwefel_t(z[i] + 4.209687462275036e+002, n);
+        for (int i = t; i < n; i += 4) a += schwefel_t(Z(i) + 4.209687462275036e+002, n);
         return qsum(a) + 4.189828872724338e+002 * n;
     case B_SCHAFFER_F7: {
         for (int i = t; i < n - 1; i += 4) {
-            const double zi = sqrt(z[i] * z[i] + z[i + 1] * z[i + 1]);
+            const double zi = sqrt(Z(i) * Z(i) + Z(i + 1) * Z(i + 1));
             const double s = sin(50.0 * pow(zi, 0.2));
             a += sqrt(zi) + sqrt(zi) * s * s;
         }
@@ -712,23 +715,29 @@ __device__ inline double cec_basic_quad(int b, const double* z, int n, int t, co
         return n > 1 ? a * a / (n - 1) / (n - 1) : a * a;
     }
     case B_GRIE_ROSEN:
-        for (int i = t; i < n; i += 4) a += grie_rosen_t(z[i], z[i + 1 < n ? i + 1 : 0]);
+        for (int i = t; i < n; i += 4) a += grie_rosen_t(Z(i), Z(i + 1 < n ? i + 1 : 0));
         return qsum(a);
     default: {  // B_GRIEWANK
         double pr = 1.0;
         for (int i = t; i < n; i += 4) {
-            a += z[i] * z[i];
-            pr *= cos(z[i] / sqrt(1.0 + i));
+            a += Z(i) * Z(i);
+            pr *= cos(Z(i) / sqrt(1.0 + i));
         }
         return 1.0 + qsum(a) / 4000.0 - qprod(pr);
     }
     }
 }
 
+__device__ __forceinline__ double cec_basic_quad(int b, const double* z, int n, int t, const double* ew) {
+    return cec_basic_quad_t(b, [z](int i) { return z[i]; }, n, t, ew);
+}
+
 // F_fn of the warp's 8 rows X[q] (stride xs, zero-padded to n4); W: second
 // row buffer (hybrids, compositions).  X is overwritten except for
 // compositions.  Every lane of quad q returns candidate q's fitness.
-template <int NT>
+// DIRECT_UNROT: compositions evaluate unrotated components straight from the candidate (k_cec_eval);
+// false keeps the register-lean one-component-at-a-time loop (the 3-CTA/SM batch kernel).
+template <int NT, bool DIRECT_UNROT = true>
 __device__ inline double cec_eval_quad(const CecData& C, double* X, const double* src, int xs, int n, int lane,
                                        const double* ew, const double* bsm = nullptr, int bsm_comp = 0) {
     // bsm: shared-memory copy (row stride 8 NT + 4) of rotation `bsm_comp`, the others via L1.
@@ -783,33 +792,82 @@ __device__ inline double cec_eval_quad(const CecData& C, double* X, const double
     } else {
         double fit[6], wk[6];
         int inf_at = -1;
-        for (int k = 0; k < S.ncomp; k++) {
-            const int b = S.basic[k];
-            const double sc = cec_scale(b), off = cec_offset(b);
-            const double* o = C.shift + (size_t)k * n;
-            const bool rot = S.rflag[k] != 0;
-            if (k > 0) {  // the candidate again (L2-resident: k_cec_eval just streamed it in)
-                for (int i = t; i < n; i += 4) x[i] = src ? src[i] : 0.0;
+        if constexpr (DIRECT_UNROT) {
+            unsigned zero_d2 = 0;
+            bool x_intact = true;  // X still holds the candidate (a rotation overwrites it)
+            // unrotated components first, evaluated straight from the candidate through an on-the-fly
+            // affine map; rotated ones after (transform + DMMA rotation in place, re-reading the
+            // candidate from L2 when an earlier rotation consumed it)
+            for (int pass = 0; pass < 2; pass++) {
+                for (int k = 0; k < S.ncomp; k++) {
+                    const bool rot = S.rflag[k] != 0;
+                    if (rot != (pass == 1)) continue;
+                    const int b = S.basic[k];
+                    const double sc = cec_scale(b), off = cec_offset(b);
+                    const double* o = C.shift + (size_t)k * n;
+                    double d2 = 0.0;
+                    if (!rot) {
+                        for (int i = t; i < n; i += 4) {
+                            const double dv = x[i] - o[i];
+                            d2 += dv * dv;
+                        }
+                        d2 = qsum(d2);
+                        fit[k] = S.lam[k] * cec_basic_quad_t(b, [x, o, sc, off](int i) { return (x[i] - o[i]) * sc + off; },
+                                                             n, t, ew) + S.bias[k];
+                    } else {
+                        if (!x_intact) {
+                            for (int i = t; i < n; i += 4) x[i] = src ? src[i] : 0.0;
+                            __syncwarp();
+                        }
+                        for (int i = t; i < n; i += 4) {
+                            const double dv = x[i] - o[i];
+                            d2 += dv * dv;
+                            x[i] = dv * sc;
+                        }
+                        d2 = qsum(d2);
+                        __syncwarp();
+                        const bool sm = bsm && bsm_comp == k;
+                        cec_rotate_quad<NT>(sm ? bsm : C.rot_pad + (size_t)k * n4 * (8 * NT), X, xs, n, off, lane,
+                                            sm ? 8 * NT + 4 : 8 * NT);
+                        fit[k] = S.lam[k] * cec_basic_quad(b, x, n, t, ew) + S.bias[k];
+                        x_intact = false;
+                    }
+                    __syncwarp();
+                    wk[k] = d2 != 0.0 ? sqrt(1.0 / d2) * exp(-d2 / 2.0 / n / (S.sigma[k] * S.sigma[k]))
+                                      : __longlong_as_double(0x7ff0000000000000LL);
+                    if (d2 == 0.0) zero_d2 |= 1u << k;
+                }
+            }
+            if (zero_d2) inf_at = __ffs(zero_d2) - 1;  // the first such component, as the oracle scans them
+        } else {  // one component at a time, re-reading the candidate (register-lean: batch kernel)
+            for (int k = 0; k < S.ncomp; k++) {
+                const int b = S.basic[k];
+                const double sc = cec_scale(b), off = cec_offset(b);
+                const double* o = C.shift + (size_t)k * n;
+                const bool rot = S.rflag[k] != 0;
+                if (k > 0) {  // the candidate again (L2-resident: k_cec_eval just streamed it in)
+                    for (int i = t; i < n; i += 4) x[i] = src ? src[i] : 0.0;
+                    __syncwarp();
+                }
+                double d2 = 0.0;
+                for (int i = t; i < n; i += 4) {
+                    const double dv = x[i] - o[i];
+                    d2 += dv * dv;
+                    x[i] = rot ? dv * sc : dv * sc + off;
+                }
+                d2 = qsum(d2);
                 __syncwarp();
+                if (rot) {
+                    const bool sm = bsm && bsm_comp == k;
+                    cec_rotate_quad<NT>(sm ? bsm : C.rot_pad + (size_t)k * n4 * (8 * NT), X, xs, n, off, lane,
+                                        sm ? 8 * NT + 4 : 8 * NT);
+                }
+                fit[k] = S.lam[k] * cec_basic_quad(b, x, n, t, ew) + S.bias[k];
+                __syncwarp();
+                wk[k] = d2 != 0.0 ? sqrt(1.0 / d2) * exp(-d2 / 2.0 / n / (S.sigma[k] * S.sigma[k]))
+                                  : __longlong_as_double(0x7ff0000000000000LL);
+                if (d2 == 0.0 && inf_at < 0) inf_at = k;
             }
-            double d2 = 0.0;
-            for (int i = t; i < n; i += 4) {
-                const double dv = x[i] - o[i];
-                d2 += dv * dv;
-                x[i] = rot ? dv * sc : dv * sc + off;
-            }
-            d2 = qsum(d2);
-            __syncwarp();
-            if (rot) {
-                const bool sm = bsm && bsm_comp == k;
-                cec_rotate_quad<NT>(sm ? bsm : C.rot_pad + (size_t)k * n4 * (8 * NT), X, xs, n, off, lane,
-                                    sm ? 8 * NT + 4 : 8 * NT);
-            }
-            fit[k] = S.lam[k] * cec_basic_quad(b, x, n, t, ew) + S.bias[k];
-            __syncwarp();
-            wk[k] = d2 != 0.0 ? sqrt(1.0 / d2) * exp(-d2 / 2.0 / n / (S.sigma[k] * S.sigma[k]))
-                              : __longlong_as_double(0x7ff0000000000000LL);
-            if (d2 == 0.0 && inf_at < 0) inf_at = k;
         }
         double wmax = 0.0, wsum_ = 0.0;
         for (int k = 0; k < S.ncomp; k++)

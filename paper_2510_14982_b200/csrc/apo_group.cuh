@@ -708,13 +708,13 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
                     double fq = 0.0;
                     const int nt = cec_nt_dev(P.dim);
                     if constexpr (MAXC == 1) {
-                        fq = nt == 2 ? cec_eval_quad<2>(O.cec, g.T, src, ts, P.dim, lane, ew)
-                                     : cec_eval_quad<4>(O.cec, g.T, src, ts, P.dim, lane, ew);
+                        fq = nt == 2 ? cec_eval_quad<2, false>(O.cec, g.T, src, ts, P.dim, lane, ew)
+                                     : cec_eval_quad<4, false>(O.cec, g.T, src, ts, P.dim, lane, ew);
                     } else if constexpr (MAXC == 2) {
-                        fq = nt == 7 ? cec_eval_quad<7>(O.cec, g.T, src, ts, P.dim, lane, ew)
-                                     : cec_eval_quad<13>(O.cec, g.T, src, ts, P.dim, lane, ew);
+                        fq = nt == 7 ? cec_eval_quad<7, false>(O.cec, g.T, src, ts, P.dim, lane, ew)
+                                     : cec_eval_quad<13, false>(O.cec, g.T, src, ts, P.dim, lane, ew);
                     } else if constexpr (MAXC == 4) {
-                        fq = cec_eval_quad<13>(O.cec, g.T, src, ts, P.dim, lane, ew);
+                        fq = cec_eval_quad<13, false>(O.cec, g.T, src, ts, P.dim, lane, ew);
                     }
                     cec_f = __shfl_sync(kFull, fq, (lane & 7) * 4);  // lane q < 8 <- quad q
                 } else {
