@@ -548,7 +548,7 @@ struct apo_run {
 
 extern "C" {
 
-int apo_abi_version(void) { return 1; }
+int apo_abi_version(void) { return 2; }  // 2: rng arguments, shard/load/threshold entry points
 
 const char* apo_last_error(void) { return g_err.c_str(); }
 
