@@ -220,7 +220,7 @@ def cmd_report(args) -> int:
 
 
 def read_image(path) -> "np.ndarray":
-    """8-bit grey image from .npy or binary PGM (P5); other formats are out of scope."""
+    """8-bit grey image from .npy or PGM/PPM (imaging.load_image_file)."""
     import numpy as np
 
     if str(path).endswith(".npy"):
@@ -228,33 +228,12 @@ def read_image(path) -> "np.ndarray":
         if img.ndim != 2 or img.dtype != np.uint8:
             raise ImageError(f"{path}: expected a 2-D uint8 array")
         return img
-    with open(path, "rb") as fh:
-        data = fh.read()
-    fields, pos = [], 0
-    while len(fields) < 4:  # magic, width, height, maxval; '#' comments allowed
-        while pos < len(data) and chr(data[pos]).isspace():
-            pos += 1
-        if pos < len(data) and data[pos:pos + 1] == b"#":
-            pos = data.find(b"\n", pos)
-            if pos < 0:
-                raise ImageError(f"{path}: truncated header")
-            continue
-        end = pos
-        while end < len(data) and not chr(data[end]).isspace():
-            end += 1
-        if end == pos:
-            raise ImageError(f"{path}: truncated header")
-        fields.append(data[pos:end])
-        pos = end
-    if fields[0] != b"P5":
-        raise ImageError(f"{path}: only binary PGM (P5) or .npy images are supported")
-    w, h, maxval = (int(f) for f in fields[1:])
-    if not (w > 0 and h > 0 and 0 < maxval < 256):
-        raise ImageError(f"{path}: unsupported geometry or maxval")
-    body = data[pos + 1:pos + 1 + w * h]
-    if len(body) != w * h:
-        raise ImageError(f"{path}: truncated pixel data")
-    return np.frombuffer(body, dtype=np.uint8).reshape(h, w)
+    from .imaging import ImageFormatError, load_image_file
+
+    try:
+        return load_image_file(path).pixels
+    except ImageFormatError as exc:
+        raise ImageError(f"{path}: {exc}") from None
 
 
 def cmd_threshold(args) -> int:
@@ -319,7 +298,7 @@ def build_parser() -> argparse.ArgumentParser:
     b.add_argument("--format", choices=("csv", "json"), default=None)
     b.set_defaults(handler=cmd_bench)
     t = sub.add_parser("threshold", help="multilevel Otsu / Kapur thresholds of an image")
-    t.add_argument("--image", required=True, help=".npy (uint8 2-D) or binary PGM (P5)")
+    t.add_argument("--image", required=True, help=".npy (uint8 2-D) or PGM/PPM (P2/P3/P5/P6)")
     t.add_argument("--levels", type=_int_at_least(1), default=1)
     t.add_argument("--method", choices=("otsu", "kapur"), default="otsu")
     t.add_argument("--ps", type=_int_at_least(1), default=100)

@@ -207,3 +207,109 @@ def multilevel_value(counts, thresholds, method: str = "otsu") -> float:
 
     obj = multilevel_objective(counts, len(thresholds), method)
     return -float(evaluate_batch(obj, np.asarray(thresholds, dtype=np.float64)[None, :])[0])
+
+
+# ---------------------------------------------------------------------------
+# Netpbm ingestion (API parity with imaging.py:78-194 of the reference; SURVEY.md
+# §8f item 3).  Host-side parsing -- the pixels then go to the GPU histogram.
+
+class ImageFormatError(ValueError):
+    """Malformed or unsupported PGM/PPM data; ``offset`` is the byte where parsing failed."""
+
+    def __init__(self, message: str, offset: int):
+        super().__init__(f"{message} (at byte {offset})")
+        self.offset = offset
+
+
+_WS = b" \t\n\r\x0b\x0c"
+
+
+def _tokens(data: bytes):
+    """Yield (token, offset) over a Netpbm header/ASCII raster: whitespace and '#' comments skipped."""
+    pos, n = 0, len(data)
+    while True:
+        while pos < n:
+            c = data[pos:pos + 1]
+            if c == b"#":
+                while pos < n and data[pos:pos + 1] not in (b"\n", b"\r"):
+                    pos += 1
+            elif c in _WS:
+                pos += 1
+            else:
+                break
+        if pos >= n:
+            yield None, n
+            return
+        start = pos
+        while pos < n and data[pos:pos + 1] not in _WS and data[pos:pos + 1] != b"#":
+            pos += 1
+        yield data[start:pos], start
+
+
+def load_image(data: bytes) -> GrayImage:
+    """PGM (P2/P5) or PPM (P3/P6) bytes, maxval 255, to a grey image (colour by BT.601 luminance,
+    rounded half up).  Errors carry the byte offset of the first problem."""
+    if not isinstance(data, (bytes, bytearray)):
+        raise TypeError("load_image expects bytes")
+    data = bytes(data)
+    toks = _tokens(data)
+
+    def need(what):
+        tok, off = next(toks)
+        if tok is None:
+            raise ImageFormatError(f"unexpected end of data while reading {what}", off)
+        return tok, off
+
+    def unsigned(what):
+        tok, off = need(what)
+        if not tok.isdigit():
+            raise ImageFormatError(f"expected an unsigned integer for {what}, got {tok[:20]!r}", off)
+        return int(tok), off
+
+    magic, off = need("the format magic")
+    if magic not in (b"P2", b"P3", b"P5", b"P6"):
+        raise ImageFormatError(f"unsupported format magic {magic[:8]!r}; expected P2, P3, P5 or P6", off)
+    width, off = unsigned("the width")
+    if width < 1:
+        raise ImageFormatError(f"width must be >= 1, got {width}", off)
+    height, off = unsigned("the height")
+    if height < 1:
+        raise ImageFormatError(f"height must be >= 1, got {height}", off)
+    maxval, off = unsigned("the maximum value")
+    if maxval != 255:
+        raise ImageFormatError(f"only maxval 255 is supported, got {maxval}", off)
+    chans = 3 if magic in (b"P3", b"P6") else 1
+    count = width * height * chans
+    if magic in (b"P5", b"P6"):
+        pos = off + len(str(maxval))
+        if pos >= len(data) or data[pos:pos + 1] not in _WS:
+            raise ImageFormatError("expected a whitespace byte before the raster", pos)
+        raster = data[pos + 1:pos + 1 + count]
+        if len(raster) < count:
+            raise ImageFormatError(f"raster truncated: expected {count} bytes, found {len(raster)}", len(data))
+        values = np.frombuffer(raster, dtype=np.uint8).copy()
+    else:
+        values = np.empty(count, dtype=np.uint8)
+        for k in range(count):
+            v, off = unsigned("a raster value")
+            if v > 255:
+                raise ImageFormatError(f"raster value {v} exceeds maxval 255", off)
+            values[k] = v
+    if chans == 3:
+        rgb = values.reshape(height, width, 3).astype(np.float64)
+        y = np.floor(0.299 * rgb[..., 0] + 0.587 * rgb[..., 1] + 0.114 * rgb[..., 2] + 0.5)
+        return GrayImage(np.clip(y, 0.0, 255.0).astype(np.uint8))
+    return GrayImage(values.reshape(height, width))
+
+
+def load_image_file(path) -> GrayImage:
+    with open(path, "rb") as fh:
+        return load_image(fh.read())
+
+
+def write_pgm(img: GrayImage, binary: bool = True) -> bytes:
+    """P5 (default) or P2 bytes; both round-trip through load_image pixel for pixel."""
+    head = f"{'P5' if binary else 'P2'}\n{img.width} {img.height}\n255\n".encode("ascii")
+    if binary:
+        return head + img.pixels.tobytes()
+    return head + ("\n".join(" ".join(map(str, row.tolist())) for row in img.pixels) + "\n").encode("ascii")

@@ -67,7 +67,7 @@ def test_pgm_reader(tmp_path):
     p.write_bytes(b"P5\n# comment\n4 3\n255\n" + img.tobytes())
     assert np.array_equal(cli.read_image(p), img)
     q = tmp_path / "b.pgm"
-    q.write_bytes(b"P2\n4 3\n255\n" + b"0 " * 12)
+    q.write_bytes(b"P2\n4 3\n254\n" + b"0 " * 12)
     assert cli.main(["threshold", "--image", str(q)]) == 4
 
 
