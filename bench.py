@@ -216,7 +216,9 @@ def c4_measure(args, name, rank, world, local, K, W):
     from paper_2510_14982_b200.engine import DeviceRun
 
     ps, dim = args.ps, args.dim
-    T = max(100, K + W)
+    # the run is exactly W + K iterations long, so the K timed steps carry the schedule (p_ah, f, decay:
+    # numba_backend.py:357-366) from early autotroph-heavy iterations to the heterotroph-heavy end
+    T = W + K
     obj = pz.get_objective(name)
     cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=T, seed=rank)
     run = DeviceRun(cfg, obj)
@@ -300,7 +302,8 @@ def bench_ours(args, rank, world, local):
         "dtype": "f64", "data": "synthetic (keyed-hash initial population, seed = rank; synthetic CEC2022 "
                                 "shift/rotation/shuffle data, cec2022.py)",
         "config": {"workload": c4_workload(args.objective, ps, dim), "ps": ps, "dim": dim,
-                   "iterations_per_step": 1, "max_iterations": max(100, K + W),
+                   "iterations_per_step": 1, "max_iterations": K + W,
+                   "schedule": "the K timed steps are the last K of a (W+K)-iteration run (autotroph -> heterotroph)",
                    "l2": "inputs larger than L2 (2 x 800 MB population buffers)",
                    "parallelism": f"independent populations x{world} (seed = rank)" if world > 1 else "single GPU",
                    "rng": "keyed fmix64 (bit-exact with the reference)"},
@@ -342,7 +345,7 @@ def bench_sharded(args, rank, world, local, K, W):
     from paper_2510_14982_b200.shard import ShardedRun
 
     ps, dim = args.ps, args.dim
-    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=max(100, K + W), seed=0)
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=K + W, seed=0)
     run = ShardedRun(cfg, args.objective)
     run.initialize()
     run.iterate(W)
@@ -370,11 +373,14 @@ def bench_e2e(cfg, obj, K, rank, world):
 
     import paper_2510_14982_b200 as pz
 
-    pop = pz.initialize(cfg, obj)
+    import dataclasses
+
     W = 4  # warm-up: lazy init, first-touch of host pages, the two page-locked buffers step() alternates
+    n = 10
+    cfg = dataclasses.replace(cfg, max_iterations=W + n)
+    pop = pz.initialize(cfg, obj)
     for t in range(W):
         pop = pz.step(pop, cfg, obj, t)
-    n = 10
     torch.cuda.synchronize()
     barrier(world)
     per = []
@@ -585,7 +591,7 @@ def bench_reference(args, rank, world):
     import paper_2510_14982_b200 as pz
 
     ps, dim, K, W = args.ps, args.dim, args.steps, args.warmup
-    T = max(100, K + W)
+    T = W + K  # the same schedule span as the GPU arm
     nthreads = os.cpu_count() or 1
     pos, fit = oracle.initialize(0, ps, dim, -100.0, 100.0, args.objective)
     step_args = dict(seed=0, max_iterations=T, name=args.objective, lower=-100.0, upper=100.0, nthreads=nthreads)

@@ -15,9 +15,10 @@ rng = sys.argv[4] if len(sys.argv) > 4 else "keyed"
 cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=100, seed=0, rng=rng)
 run = DeviceRun(cfg, pz.get_objective(name))
 run.initialize()
-run.iterate(3)
+skip = int(sys.argv[5]) if len(sys.argv) > 5 else 3
+run.iterate(skip)
 torch.cuda.synchronize()
 run.profile(True)
 run.iterate(5)
 a, b, n = run.profile_split()
-print(f"{name} D={dim} ps={ps} rng={rng}: candidates {a / n:.3f} ms  evaluate {b / n:.3f} ms  per iteration")
+print(f"{name} D={dim} ps={ps} rng={rng} from iteration {skip}: candidates {a / n:.3f} ms  evaluate {b / n:.3f} ms  per iteration")
