@@ -12,6 +12,8 @@
 //            candidate, clamp, fitness (eval_warp), greedy select and the kept
 //            row written straight from registers.
 #pragma once
+#include <type_traits>
+
 #include "apo_update.cuh"
 
 namespace apo {
@@ -521,7 +523,9 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
     double carry = 0.0;  // candidate at d-1 for lane 0 of the next chunk
 
     auto mk = [&](int d) -> double { return ((mb[d >> 5] >> (d & 31)) & 1u) ? 1.0 : 0.0; };
-    auto forage = [&](int d, double xd, double aj, double am, double ap) -> double {
+    // AUTO: compile-time operation for the unrolled paths (-1: decided at run time from op)
+    auto forage_t = [&](auto auto_tag, int d, double xd, double aj, double am, double ap) -> double {
+        constexpr int AUTO = decltype(auto_tag)::value;
         double acc = 0.0;
         acc = acc + w0 * (am - ap);
         double ep = acc;
@@ -530,13 +534,17 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
             ep = acc / npd;
         }
         double direction;
-        if (op == OP_AUTOTROPH) {
+        const bool is_auto = AUTO == 1 || (AUTO < 0 && op == OP_AUTOTROPH);
+        if (is_auto) {
             direction = (aj - xd) + ep;
         } else {
             const double uv = uniform(base, kVectorBase + (uint64_t)d);
             direction = ((1.0 + (sgn * uv) * P.decay) * xd - xd) + ep;
         }
         return xd + (f * direction) * mk(d);
+    };
+    auto forage = [&](int d, double xd, double aj, double am, double ap) -> double {
+        return forage_t(std::integral_constant<int, -1>{}, d, xd, aj, am, ap);
     };
     // every lane calls finish() once per chunk (the shuffles need the full warp)
     // CO (candidates only, CEC2022 on HBM): no fitness terms; only rosenbrock needs the d-1 neighbour
@@ -556,8 +564,10 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
         }
     };
 
-    if (MAXC > 0 && op == OP_AUTOTROPH) {
-        // row loads issued LC chunks at a time (4 rows x LC chunks in flight)
+    // the two foraging operations (95% of protozoa), each with its own unrolled body: row loads issued
+    // LC chunks at a time (up to 4 rows x LC chunks in flight) and the chunks' arithmetic interleaved
+    auto unrolled = [&](auto auto_tag) {
+        constexpr bool AUTO = decltype(auto_tag)::value == 1;
         constexpr int LC = (APO_LOAD_CHUNKS < MAXC ? APO_LOAD_CHUNKS : (MAXC > 0 ? MAXC : 1));
 #pragma unroll
         for (int c0 = 0; c0 < (MAXC > 0 ? MAXC : 1); c0 += LC) {
@@ -567,7 +577,7 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
                 const int d = lane + 32 * (c0 + u);
                 if (d < dim) {
                     xv[u] = x[d];
-                    aj[u] = xj[d];
+                    aj[u] = AUTO ? xj[d] : 0.0;
                     am[u] = xm[d];
                     ap[u] = xp[d];
                 }
@@ -576,9 +586,16 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
             for (int u = 0; u < LC; u++) {
                 const int c = c0 + u;
                 const int d = lane + 32 * c;
-                if (32 * c < dim) finish(d, d < dim ? forage(d, xv[u], aj[u], am[u], ap[u]) : 0.0, d < dim);
+                if (32 * c < dim) finish(d, d < dim ? forage_t(auto_tag, d, xv[u], aj[u], am[u], ap[u]) : 0.0, d < dim);
             }
         }
+    };
+    // candidates-only kernels (no fitness code) afford a second unrolled body for the heterotroph; the
+    // fused kernels keep one (register pressure: measured 50% slower with both)
+    if (MAXC > 0 && op == OP_AUTOTROPH) {
+        unrolled(std::integral_constant<int, 1>{});
+    } else if (CO && MAXC > 0 && op == OP_HETEROTROPH) {
+        unrolled(std::integral_constant<int, 0>{});
     } else {
         const int nch = (dim + 31) / 32;
         for (int c = 0; c < nch; c++) {
