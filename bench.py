@@ -328,6 +328,7 @@ def bench_ours(args, rank, world, local):
         result["e2e"] = bench_e2e(m["cfg"], m["obj"], K, rank, world)
         result["e2e_run"] = bench_e2e_run(m["cfg"], m["obj"], rank, world)
     if not args.no_suite and rank == 0:
+        result["suite_c1"] = bench_c1()
         result["suite_c2"] = bench_suite(world)
         result["suite_c3"] = bench_c3()
         result["suite_c5"] = bench_c5()
@@ -448,6 +449,35 @@ def bench_suite(world):
             "workload": "C2: CEC2022 F1-F12 (synthetic data) x 30 seeds, D=20, ps=100, T=1000, one CTA per run",
             "median_best_minus_fstar": [float(np.median(best[k]) - pz.cec2022.FSTAR[k]) for k in range(12)],
             "gpus": 1}
+
+
+def bench_c1():
+    """BASELINE config 1: CEC2022 F1 D=10, pop=50, 1000 iterations, one seed -- a latency regime (one CTA
+    holds the whole run in shared memory); the oracle's single-threaded run of the same config beside it."""
+    import torch
+
+    import paper_2510_14982_b200 as pz
+
+    cfg = pz.ApoConfig(ps=50, dim=10, bounds=pz.Bounds(-100.0, 100.0, 10), max_iterations=1000, seed=0)
+    pz.run(cfg, "cec2022_f1")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = pz.run(cfg, "cec2022_f1")
+    gpu_s = time.perf_counter() - t0
+    out = {"workload": "C1: CEC2022 F1 (synthetic data) D=10, ps=50, T=1000, seed 0, pz.run end to end",
+           "seconds": gpu_s, "value": cfg.ps * (cfg.max_iterations + 1) / gpu_s, "unit": UNIT,
+           "best_minus_fstar": res.best_fitness - 300.0}
+    try:
+        import oracle
+
+        t0 = time.perf_counter()
+        want = oracle.run(ps=50, dim=10, max_iterations=1000, seed=0, name="cec2022_f1", lower=-100.0, upper=100.0)
+        cpu_s = time.perf_counter() - t0
+        out["cpu_oracle_seconds"] = cpu_s
+        out["cpu_oracle_best_minus_fstar"] = want["best_fitness"] - 300.0
+    except Exception as exc:  # the oracle is a checker; its absence must not cost the GPU line
+        out["cpu_oracle"] = f"unavailable: {exc}"[:200]
+    return out
 
 
 def bench_c3():
