@@ -1,0 +1,31 @@
+"""Small end-to-end exercise of every kernel family for compute-sanitizer (not a test of values)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2510_14982_b200 as pz
+from paper_2510_14982_b200 import engine, imaging
+from paper_2510_14982_b200.shard import ShardedRun
+
+for name, ps, dim in [("rosenbrock", 300, 37), ("cec2022_f6", 700, 50), ("cec2022_f10", 300, 20),
+                      ("cec2022_f1", 300, 150), ("griewank", 200, 300), ("cec2022_f12", 260, 120)]:
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=4, seed=1)
+    engine.BATCH_PS_LIMIT = 256
+    pz.run(cfg, name)                      # batch (if it fits) or device loop
+    engine.BATCH_PS_LIMIT = 0
+    pz.run(cfg, name)                      # device loop
+    pop = pz.initialize(cfg, name)
+    pz.step(pop, cfg, name, 0)             # reference-facing path
+    if dim <= 256:
+        sh = ShardedRun(cfg, name, virtual_world=3)
+        sh.initialize()
+        sh.iterate(2)
+        sh.close()
+img = (np.arange(64 * 64) % 251).astype(np.uint8).reshape(64, 64)
+pz.apo_multithreshold(img, 3, "kapur", ps=40, iterations=5)
+pz.run(pz.ApoConfig(ps=64, dim=8, bounds=pz.Bounds(-5.0, 5.0, 8), max_iterations=5, rng="philox"), "cec2022_f4")
+torch.cuda.synchronize()
+print("sanitize exercise done")
