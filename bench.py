@@ -164,6 +164,15 @@ def profile_traffic(workload: str, objective: str):
         return None
 
 
+def dmma_pipe_pct(workload: str, objective: str):
+    """DMMA pipe utilisation of the evaluation kernel from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get("dmma_pipe_active_pct", {}).get(f"{workload}:{objective}")
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 # algorithmic bytes (SURVEY.md section 8(d))
 
@@ -277,7 +286,8 @@ def c4_measure(args, name, rank, world, local, K, W):
                         "frac": round(tf / pk, 4), "peak_source": pk_src, "kernel_ms_avg": round(eval_ms / n, 4),
                         "kernel_share_of_step": round(eval_ms / ms, 4), "flops_per_launch": flops,
                         "flops_per_eval": nrot * 2.0 * dim * dim,
-                        "also_reads_bytes_per_eval": 8 * dim + 16, "traffic": profile_traffic("c4eval", name)})
+                        "also_reads_bytes_per_eval": 8 * dim + 16, "traffic": profile_traffic("c4eval", name),
+                        "ncu_dmma_pipe_active_pct": dmma_pipe_pct("c4eval", name)})
     dominant = max(kernels, key=lambda k: k["kernel_ms_avg"])
     return dict(cfg=cfg, obj=obj, ms=ms, max_ms=max_ms, clocks=clk, kernels=kernels, dominant=dominant,
                 launches=launches)

@@ -27,7 +27,12 @@ def main(path, top=25):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     h = rr[0]
-    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum",
+                 "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+                 "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+                 "sm__ops_path_tensor_src_fp64.sum.pct_of_peak_sustained_elapsed",
+                 "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                 "dram__throughput.avg.pct_of_peak_sustained_elapsed"):
         if name in h:
             print(f"  {name:38s} {rr[2][h.index(name)]} {rr[1][h.index(name)]}")
     sass = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
