@@ -1,22 +1,21 @@
-// apo_kernels.cu -- sm_100a kernels and the C ABI of libapo_b200.so.
+// apo_kernels.cu -- the small kernels and the C ABI of libapo_b200.so.
 //
 // Built with --fmad=false (oracle-exact arithmetic).
-// Kernels:
-//   k_update<INDIRECT>  fused per-protozoon update, one warp per protozoon
-//                       (numba_backend.py:141-290); dense rank-ordered rows
-//                       at the run_updates boundary, or slot-resident rows
-//                       through the rank->slot order in the device loop.
-//                       Fuses the best-so-far min (engine.py:196) and the
-//                       warning count (numba_backend.py:372).
+// Kernels defined here:
 //   k_init              iteration-0 draws + evaluation (engine.py:116-139)
 //   k_evaluate          batch fitness (objectives.py:222-228)
 //   k_make_keys         fitness -> order-preserving u64 keys for the stable
 //                       radix sort (core.py:504-513)
 //   k_dr_draw/resolve   coordinator Dr set (core.py:263-278) as a parallel
 //                       partial Fisher-Yates (see apo_update.cuh:build_mask)
-//   k_run_batch         persistent run: one CTA per independent run, the
-//                       population in shared memory for every iteration
+//   k_threshold_tables  multilevel Otsu/Kapur prefix tables
 //   k_histogram_u8      shared-memory privatised 256-bin histogram
+// The hot kernels are templates in apo_kernels.cuh, instantiated in their own
+// TUs and reached through pick_* getters:
+//   k_update_group / k_update   the fused per-protozoon update (apo_update_*.cu)
+//   k_cec_eval                  CEC2022 DMMA evaluation + select (apo_cec_eval.cu)
+//   k_run_batch                 one CTA per independent run (apo_batch_*.cu)
+//   k_cec_prep/k_dgemm_nn/k_cec_finish   large-D GEMM path (apo_cec_gemm.cu)
 #include <cub/cub.cuh>
 
 #include <cmath>
