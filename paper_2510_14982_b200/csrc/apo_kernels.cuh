@@ -290,30 +290,49 @@ __global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
     unsigned warn_total = 0;
     int cur = 0;
     for (int t = 0; t < A.n_iters; t++) {
-        // 1. stable sort by fitness, ties by previous rank (core.py:504-513)
-        for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) {
-            const unsigned long long k = keys[sl];
-            const int pr = rankof[sl];
+        // 1. stable sort by fitness, ties by previous rank (core.py:504-513): each rank is a count of
+        //    smaller keys, S lanes per element (S a power of two, the counts folded by shuffles); the
+        //    coordinator draws (2.) run meanwhile on the last warp when the sort leaves it idle
+        const uint64_t key_it = (uint64_t)t + 1;
+        const int dr_warp = nwarps - 1;
+#ifndef APO_BATCH_OVERLAP
+#define APO_BATCH_OVERLAP 1
+#endif
+        const bool dr_overlap = APO_BATCH_OVERLAP && ps <= 32 * dr_warp;
+        auto coordinator = [&]() {  // core.py:263-278
+            const Key cbase = stream_key(A.rng, seed, key_it, kCoordinator);
+            const double pf = A.pf_max * uniform(cbase, 0);
+            const int count = (int)ceil((double)ps * pf);
+            build_mask(ps, count, cbase, 1, cs, lane);
+        };
+        if (dr_overlap && warp == dr_warp) coordinator();
+        const int span = dr_overlap ? 32 * dr_warp : (int)blockDim.x;
+        int S = 1;
+        while (APO_BATCH_OVERLAP && S < 8 && 2 * S * ps <= span) S <<= 1;
+        for (int base_t = 0; base_t < ps * S; base_t += span) {
+            const int tt = base_t + (int)threadIdx.x;
             int cnt = 0;
-            for (int q = 0; q < ps; q++) {
-                const unsigned long long kq = keys[q];
-                cnt += (kq < k) || (kq == k && rankof[q] < pr);
+            int sl = tt / S;
+            const bool act = (int)threadIdx.x < span && sl < ps;
+            if (act) {
+                const unsigned long long k = keys[sl];
+                const int pr = rankof[sl];
+                for (int q = tt % S; q < ps; q += S) {
+                    const unsigned long long kq = keys[q];
+                    cnt += (kq < k) || (kq == k && rankof[q] < pr);
+                }
             }
-            newrank[sl] = cnt;
+            if ((int)threadIdx.x < span) {  // whole warps: span is a multiple of 32 and S divides 32
+                for (int o = 1; o < S; o <<= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+                if (act && tt % S == 0) newrank[sl] = cnt;
+            }
         }
         __syncthreads();
         for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) {
             order[newrank[sl]] = sl;
             rankof[sl] = newrank[sl];
         }
-        // 2. coordinator draws (core.py:263-278)
-        const uint64_t key_it = (uint64_t)t + 1;
-        if (warp == 0) {
-            const Key cbase = stream_key(A.rng, seed, key_it, kCoordinator);
-            const double pf = A.pf_max * uniform(cbase, 0);
-            const int count = (int)ceil((double)ps * pf);
-            build_mask(ps, count, cbase, 1, cs, lane);
-        }
+        if (!dr_overlap && warp == 0) coordinator();
         __syncthreads();
         // 3. fused updates
         IterParams P;
