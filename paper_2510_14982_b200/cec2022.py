@@ -84,6 +84,8 @@ MIN_DIM = (2, 2, 2, 2, 2, 2, 5, 5, 2, 2, 2, 2)
 
 
 def cec2022_objective(fn: int, data_seed: int = 2022, rotation: str = "dmma") -> Objective:
+    if not (isinstance(fn, int) and 1 <= fn <= 12):
+        raise ValueError(f"CEC2022 function index must be 1..12, got {fn!r}")
     if rotation not in ("dmma", "fma"):
         raise ValueError(f"rotation must be 'dmma' or 'fma', got {rotation!r}")
     name = f"cec2022_f{fn}" + ("" if rotation == "dmma" else "_fma")

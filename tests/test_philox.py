@@ -134,3 +134,24 @@ def test_philox_best_fitness_distribution_matches_reference_stream(name, dim):
                           want_trace=False).best_fitness
     p = mannwhitneyu(keyed, philox, alternative="two-sided").pvalue
     assert p > 1e-3, f"{name}: keyed median {np.median(keyed):.6g} vs philox {np.median(philox):.6g}, p = {p:.2e}"
+
+
+@pytest.mark.gpu
+def test_philox_sharded_partitions_equal_device_loop():
+    """Production mode keeps partition independence (every draw keyed by seed, iteration, rank, slot)."""
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200 import engine
+    from paper_2510_14982_b200.shard import ShardedRun
+
+    cfg = pz.ApoConfig(ps=1000, dim=30, bounds=pz.Bounds(-100.0, 100.0, 30), max_iterations=8, seed=3, rng="philox")
+    sh = ShardedRun(cfg, "cec2022_f4", virtual_world=3)
+    sh.initialize()
+    sh.iterate(8)
+    pos, fit = sh.population()
+    sh.close()
+    run = engine.DeviceRun(cfg, pz.get_objective("cec2022_f4"))
+    run.initialize()
+    run.iterate(8)
+    pos1, fit1 = run.population()
+    run.close()
+    assert np.array_equal(fit, fit1) and np.array_equal(pos, pos1)

@@ -194,3 +194,17 @@ def test_concurrent_stream_batches_match_sequential():
     torch.cuda.synchronize()
     for o, s in zip(outs, seq):
         assert np.array_equal(o.best_fitness.cpu().numpy(), s)
+
+
+@pytest.mark.gpu
+def test_max_threshold_count_matches_oracle():
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200 import imaging
+
+    counts = np.bincount(synthetic_image(256).ravel(), minlength=256)
+    for method in ("otsu", "kapur"):
+        obj = imaging.multilevel_objective(counts, 32, method)
+        x = np.random.default_rng(5).uniform(0.0, 255.0, size=(64, 32))
+        got = pz.evaluate_batch(obj, x)
+        want = np.array([oracle.threshold_eval(method, r, obj.table) for r in x])
+        np.testing.assert_allclose(got, want, rtol=KAPUR_RTOL)
