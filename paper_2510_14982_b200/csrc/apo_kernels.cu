@@ -1372,12 +1372,22 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     A.warnings = (long long*)warnings;
     A.rng = rng;
     batch_smem_needs(objectives_host, nruns, dim, &A.cec_bufs, &A.tab_smem);
-    const BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs, A.tab_smem);
+    BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs, A.tab_smem);
     APO_CHECK((int64_t)L.total + 2048 <= smem_optin(), "population too large for the shared-memory batch kernel");
+    // fewer runs than SMs: each run owns an SM, so give it twice the warps (k_run_batch's comment)
+    static const int env_threads = getenv("APO_BATCH_THREADS") ? atoi(getenv("APO_BATCH_THREADS")) : 0;
+    int threads = kThreads;
+    if (env_threads == kBatchWideThreads || (env_threads == 0 && nruns <= num_sms() && ps > (int64_t)kWarps)) {
+        const BatchLayout W = batch_layout(A.ps, A.dim, A.ld, kBatchWideThreads / 32, A.cec_bufs, A.tab_smem);
+        if ((int64_t)W.total + 2048 <= smem_optin()) {
+            L = W;
+            threads = kBatchWideThreads;
+        }
+    }
     const void* fn = pick_run_batch((int)dim);
     if (int rc = set_smem(fn, L.total)) return rc;
     void* args[] = {(void*)&A};
-    APO_CUDA(cudaLaunchKernel(fn, dim3((unsigned)nruns), dim3(kThreads), args, L.total, st));
+    APO_CUDA(cudaLaunchKernel(fn, dim3((unsigned)nruns), dim3((unsigned)threads), args, L.total, st));
     APO_CUDA(cudaGetLastError());
     cudaFreeAsync(d_descs, st);
     return APO_OK;

@@ -226,9 +226,16 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
 }
 
 // MAXC >= 0: group path (apo_group.cuh); MAXC < 0: warp-per-protozoon (dim > 256).
-// 3 CTAs/SM: the C2 suite (360 runs) then fits one wave on 148 SMs.
+// Launched with kThreads when the batch fills the GPU (80 registers: 3 CTAs/SM, so the C2 suite's 360
+// runs fit one wave on 148 SMs) and with kBatchWideThreads when there are fewer runs than SMs: a run is
+// then latency-bound (one SM, ~2 warps per scheduler at 256 threads) and twice the warps halve the
+// protozoa each warp walks per iteration.
+constexpr int kBatchWideThreads = 512;
+#ifndef APO_BATCH_MAXNREG
+#define APO_BATCH_MAXNREG 80
+#endif
 template <int MAXC>
-__global__ void __launch_bounds__(kThreads, 3) k_run_batch(BatchArgs A) {
+__global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ unsigned long long red_min[32];
     __shared__ unsigned red_warn[32];
