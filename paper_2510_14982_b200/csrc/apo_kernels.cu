@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "apo_b200.h"
@@ -331,9 +332,17 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
     if (per_sm < 1) per_sm = 1;
     if (a.rank_hi <= 0) a.rank_hi = a.P.ps;  // default: every rank
-    const long long units = group ? ((long long)(a.rank_hi - a.rank_lo) + 31) / 32 : (long long)a.P.ps;
-    const long long need = (units + w - 1) / w;
     const long long cap = (long long)per_sm * num_sms();
+    if (group) {
+        // 32 ranks per warp, or fewer when that leaves warp slots empty: a small population is
+        // latency-bound and each warp walks its group's ranks partly in sequence
+        const long long ranks = a.rank_hi - a.rank_lo, slots = cap * w;
+        static const int env_g = getenv("APO_GROUP_SIZE") ? atoi(getenv("APO_GROUP_SIZE")) : 0;
+        long long G = env_g > 0 ? env_g : (ranks + slots - 1) / slots;
+        a.gsize = (int)(G < 1 ? 1 : G > 32 ? 32 : G);
+    }
+    const long long units = group ? ((long long)(a.rank_hi - a.rank_lo) + a.gsize - 1) / a.gsize : (long long)a.P.ps;
+    const long long need = (units + w - 1) / w;
     const int grid = (int)(need < cap ? need : cap);
     {
         void* args[] = {(void*)&a};
@@ -476,7 +485,8 @@ int dr_device(int rng, uint64_t seed, uint64_t key_iteration, int64_t ps, int64_
     k_dr_draw<<<grid_for(count, 256), 256, 0, st>>>((int)count, (int)ps, cbase, keys);
     APO_CUDA(cudaGetLastError());
     size_t bytes_needed = tmp_bytes;
-    APO_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes_needed, keys, keys_sorted, (int)count, 0,
+    // only the target bits: the step half is already in step order and the radix sort is stable
+    APO_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes_needed, keys, keys_sorted, (int)count, 32,
                                             32 + nbits_for(ps), st));
     k_dr_resolve<<<grid_for(count, 256), 256, 0, st>>>((int)count, (int)ps, cbase, keys_sorted, bits, bytes);
     APO_CUDA(cudaGetLastError());
@@ -500,7 +510,7 @@ void batch_smem_needs(const apo_objective* objs, int64_t n, int64_t dim, int* ce
 size_t dr_tmp_bytes(int64_t cap, int64_t ps) {
     size_t b = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, b, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                   (int)(cap > 0 ? cap : 1), 0, 32 + nbits_for(ps));
+                                   (int)(cap > 0 ? cap : 1), 32, 32 + nbits_for(ps));
     return b;
 }
 
@@ -879,20 +889,30 @@ int apo_run_iterate(apo_run* r, int64_t n) {
     APO_CHECK(n >= 0 && r->iters + n <= r->T, "iteration budget exceeded");
     cudaStream_t st = r->stream;
     const int ps = (int)r->ps;
+    static const char* env_small = getenv("APO_SMALL_PROLOGUE");
+    const bool small_prologue = prologue_small_fits(ps) && !(env_small && atoi(env_small) == 0);
     for (int64_t k = 0; k < n; k++) {
         const int64_t t = r->iters;
         const uint64_t key_it = (uint64_t)t + 1;
-        // 1. stable sort by fitness, ties by previous rank
-        k_make_keys<<<grid_for(ps, 256), 256, 0, st>>>(ps, r->fit[r->cur], r->order, r->keys_in, r->vals_in);
-        APO_CUDA(cudaGetLastError());
-        size_t tb = r->tmp_bytes;
-        APO_CUDA(cub::DeviceRadixSort::SortPairs(r->tmp, tb, r->keys_in, r->keys_out, r->vals_in, r->order, ps, 0, 64,
-                                                 st));
-        // 2. coordinator draws
         const int64_t count = (int64_t)coord_count(r->rng, r->seed, key_it, r->ps, r->pf_max);
-        if (int rc = dr_device(r->rng, r->seed, key_it, r->ps, count, r->dr_keys, r->dr_sorted, r->tmp, r->tmp_bytes,
-                               r->dr_bits, nullptr, st))
-            return rc;
+        if (small_prologue) {
+            // 1 + 2 as one launch (apo_prologue.cu); the new order goes to the spare buffer
+            APO_CUDA(launch_prologue_small(ps, r->fit[r->cur], r->order, r->vals_in, (int)count,
+                                           stream_key(r->rng, r->seed, key_it, kCoordinator), r->dr_bits,
+                                           r->keys_in, (int*)r->keys_out, num_sms(), st));
+            std::swap(r->order, r->vals_in);
+        } else {
+            // 1. stable sort by fitness, ties by previous rank
+            k_make_keys<<<grid_for(ps, 256), 256, 0, st>>>(ps, r->fit[r->cur], r->order, r->keys_in, r->vals_in);
+            APO_CUDA(cudaGetLastError());
+            size_t tb = r->tmp_bytes;
+            APO_CUDA(cub::DeviceRadixSort::SortPairs(r->tmp, tb, r->keys_in, r->keys_out, r->vals_in, r->order, ps, 0,
+                                                     64, st));
+            // 2. coordinator draws
+            if (int rc = dr_device(r->rng, r->seed, key_it, r->ps, count, r->dr_keys, r->dr_sorted, r->tmp,
+                                   r->tmp_bytes, r->dr_bits, nullptr, st))
+                return rc;
+        }
         // 3. fused update
         IterParams P;
         P.seed = r->seed;

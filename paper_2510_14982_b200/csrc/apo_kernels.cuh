@@ -41,7 +41,8 @@ struct UpdArgs {
     unsigned long long* trace_key;
     int cec_bufs;      // CEC2022 scratch rows (cec_bufs_for(code))
     uint8_t* cand_ok;  // non-null: candidates only (k_cec_eval finishes the update)
-    int rank_lo, rank_hi;  // 0-based rank range to update (rank_lo % 32 == 0); [0, ps) unless sharded
+    int rank_lo, rank_hi;  // 0-based rank range to update; [0, ps) unless sharded
+    int gsize;             // group path: consecutive ranks per warp (1..32; fewer spread small populations)
 };
 
 __device__ __forceinline__ void block_finish(unsigned long long my_min, unsigned my_warn,
@@ -143,10 +144,11 @@ __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group
     }
     unsigned long long my_min = ~0ull;
     unsigned my_warn = 0;
-    const int g_hi = (A.rank_hi + 31) >> 5;
-    for (int grp = (A.rank_lo >> 5) + blockIdx.x * nwarps + warp; grp < g_hi; grp += gridDim.x * nwarps) {
-        const int i0 = grp * 32 + 1;
-        const int n = min(32, A.rank_hi - grp * 32);
+    const int G = A.gsize;
+    const int ngroups = (A.rank_hi - A.rank_lo + G - 1) / G;
+    for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
+        const int i0 = A.rank_lo + grp * G + 1;
+        const int n = min(G, A.rank_hi - (i0 - 1));
         if constexpr (SEL) {
             const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
             update_group<MAXC, OUT_SEL, KIND>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
@@ -670,6 +672,11 @@ __host__ __device__ inline int gemm_np(int dim) { return (dim + 63) & ~63; }
 const void* pick_update_sel(int dim, bool cand_only, bool cec);
 const void* pick_update_dense(int dim, bool cand_only, bool cec);
 const void* pick_run_batch(int dim);
+// apo_prologue.cu: stable sort + Dr set as one launch for small populations (else the CUB prologue)
+bool prologue_small_fits(long long ps);
+cudaError_t launch_prologue_small(int ps, const double* fit, const int* order_in, int* order_out, int count,
+                                  Key cbase, unsigned* dr_bits, unsigned long long* scratch_keys, int* scratch_rank,
+                                  int num_sms, cudaStream_t st);
 const void* pick_cec_eval(bool sel, int dim, bool fast);
 
 }  // namespace apo

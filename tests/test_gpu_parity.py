@@ -152,6 +152,24 @@ def test_device_loop_vs_oracle_mid_size(pz, name, monkeypatch):
     assert res.best_fitness == want["best_fitness"]
 
 
+@pytest.mark.parametrize("ps,pf_max", [(1000, 1.0), (2048, 0.5), (2049, 1.0), (5000, 1.0), (12289, 0.3),
+                                        (24576, 0.1), (24577, 0.1)])
+def test_device_loop_prologue_paths_vs_oracle(pz, ps, pf_max, monkeypatch):
+    """The prologue (stable sort + Dr set) has three implementations by population size: counting in
+    one launch (ps <= 2048), tile sort + merge (<= 24576, apo_prologue.cu), CUB radix sort beyond;
+    all bit-exact, including Dr sets as large as the population (pf_max = 1)."""
+    from paper_2510_14982_b200 import engine
+
+    monkeypatch.setattr(engine, "BATCH_PS_LIMIT", 0)
+    cfg = pz.ApoConfig(ps=ps, dim=3, bounds=pz.Bounds(-5.0, 5.0, 3), max_iterations=6, seed=ps, pf_max=pf_max)
+    res = pz.run(cfg, "rosenbrock")
+    want = oracle.run(ps=ps, dim=3, max_iterations=6, seed=ps, name="rosenbrock", lower=-5.0, upper=5.0,
+                      pf_max=pf_max, nthreads=8)
+    assert np.array_equal(res.trace, want["trace"])
+    assert np.array_equal(res.population.positions, want["positions"])
+    assert np.array_equal(res.population.fitness, want["fitness"])
+
+
 def test_large_population_one_iteration_vs_oracle(pz):
     """C4 shape (ps=1M, D=100): one teacher-forced update, bit-exact."""
     import torch
