@@ -88,6 +88,13 @@ def cec2022_objective(fn: int, data_seed: int = 2022, rotation: str = "dmma") ->
         raise ValueError(f"CEC2022 function index must be 1..12, got {fn!r}")
     if rotation not in ("dmma", "fma"):
         raise ValueError(f"rotation must be 'dmma' or 'fma', got {rotation!r}")
+    return _cec2022_objective(fn, data_seed, rotation)
+
+
+@lru_cache(maxsize=None)
+def _cec2022_objective(fn: int, data_seed: int, rotation: str) -> Objective:
+    # one instance per (fn, data, rotation): its device tables (objectives.device_objective) are built
+    # once, not once per run of a batch
     name = f"cec2022_f{fn}" + ("" if rotation == "dmma" else "_fma")
     return Objective(name, CEC2022_BASE + fn, min_dim=MIN_DIM[fn - 1], data=CecFunction(fn, data_seed, rotation))
 

@@ -18,6 +18,7 @@
 //   k_cec_prep/k_dgemm_nn/k_cec_finish   large-D GEMM path (apo_cec_gemm.cu)
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -1363,11 +1364,30 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
         if (int rc = check_objective(&objectives_host[k], dim)) return rc;
     APO_CHECK(apo_run_batch_max_elems(ps, dim) > 0, "population too large for the shared-memory batch kernel");
     cudaStream_t st = as_stream(stream);
-    std::vector<ObjDesc> descs((size_t)nruns);
-    for (int64_t k = 0; k < nruns; k++) descs[(size_t)k] = to_desc(&objectives_host[k]);
-    ObjDesc* d_descs = nullptr;
-    APO_CUDA(cudaMallocAsync((void**)&d_descs, sizeof(ObjDesc) * (size_t)nruns, st));
-    APO_CUDA(cudaMemcpyAsync(d_descs, descs.data(), sizeof(ObjDesc) * (size_t)nruns, cudaMemcpyHostToDevice, st));
+    // one staging block: descriptors | claim order | claim counter
+    const size_t desc_bytes = (sizeof(ObjDesc) * (size_t)nruns + 15) & ~(size_t)15;
+    const size_t order_bytes = (4 * (size_t)nruns + 15) & ~(size_t)15;
+    std::vector<unsigned char> stage(desc_bytes + order_bytes + 16, 0);
+    ObjDesc* descs = reinterpret_cast<ObjDesc*>(stage.data());
+    for (int64_t k = 0; k < nruns; k++) descs[k] = to_desc(&objectives_host[k]);
+    {
+        // costliest runs first (per-objective cost of a D = 20 run relative to ~20 for the basic functions;
+        // measured with tools/prof_batch.py): the last claims then go to the cheap runs
+        static const float kCecCost[13] = {20, 23, 23, 24, 28, 24, 26, 58, 35, 37, 33, 58, 50};
+        auto cost = [&](int64_t k) {
+            const int c = objectives_host[k].code;
+            return c > APO_OBJ_CEC2022_BASE && c <= APO_OBJ_CEC2022_BASE + 12 ? kCecCost[c - APO_OBJ_CEC2022_BASE]
+                                                                              : 20.0f;
+        };
+        std::vector<int> ord((size_t)nruns);
+        for (int64_t k = 0; k < nruns; k++) ord[(size_t)k] = (int)k;
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost(a) > cost(b); });
+        memcpy(stage.data() + desc_bytes, ord.data(), 4 * (size_t)nruns);
+    }
+    unsigned char* d_stage = nullptr;
+    APO_CUDA(cudaMallocAsync((void**)&d_stage, stage.size(), st));
+    APO_CUDA(cudaMemcpyAsync(d_stage, stage.data(), stage.size(), cudaMemcpyHostToDevice, st));
+    ObjDesc* d_descs = reinterpret_cast<ObjDesc*>(d_stage);
     BatchArgs A;
     A.seeds = seeds;
     A.objs = d_descs;
@@ -1394,22 +1414,50 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     batch_smem_needs(objectives_host, nruns, dim, &A.cec_bufs, &A.tab_smem);
     BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs, A.tab_smem);
     APO_CHECK((int64_t)L.total + 2048 <= smem_optin(), "population too large for the shared-memory batch kernel");
-    // fewer runs than SMs: each run owns an SM, so give it twice the warps (k_run_batch's comment)
+    // Launch shape (k_run_batch's comment): more runs than SMs -> one persistent kBatchPersistThreads CTA
+    // per SM claiming runs costliest first (C2: 360 runs 1.6x faster than 3 x 256-thread CTAs per SM with
+    // one run each, whose slowest SM holds three heavy runs); a handful of runs -> one wide CTA each
+    // (latency-bound); in between -> one 256-thread CTA per run, 3 per SM, which leaves room for batches
+    // launched concurrently on other streams.  APO_BATCH_THREADS / APO_BATCH_WORKERS override (A/B runs).
     static const int env_threads = getenv("APO_BATCH_THREADS") ? atoi(getenv("APO_BATCH_THREADS")) : 0;
+    static const int env_workers = getenv("APO_BATCH_WORKERS") ? atoi(getenv("APO_BATCH_WORKERS")) : 0;
+    const int sms = num_sms();
     int threads = kThreads;
-    if (env_threads == kBatchWideThreads || (env_threads == 0 && nruns <= num_sms() && ps > (int64_t)kWarps)) {
-        const BatchLayout W = batch_layout(A.ps, A.dim, A.ld, kBatchWideThreads / 32, A.cec_bufs, A.tab_smem);
+    long long workers = 0;  // 0: one CTA per run
+    if (env_threads > 0 || env_workers > 0) {
+        if (env_threads > 0) threads = env_threads & ~31;
+        if (env_workers > 0 && env_workers < nruns) workers = env_workers;
+    } else if (nruns > sms) {
+        threads = kBatchPersistThreads;
+        workers = sms;
+    } else if (nruns <= kBatchFewRuns && ps > (int64_t)kWarps) {
+        threads = kBatchWideThreads;
+    }
+    APO_CHECK(threads >= 32 && threads <= 1024, "APO_BATCH_THREADS must be in [32, 1024]");
+    if (threads != kThreads) {
+        const BatchLayout W = batch_layout(A.ps, A.dim, A.ld, threads / 32, A.cec_bufs, A.tab_smem);
         if ((int64_t)W.total + 2048 <= smem_optin()) {
             L = W;
-            threads = kBatchWideThreads;
+        } else {  // the wide scratch does not fit: the default shape
+            threads = kThreads;
+            workers = 0;
         }
     }
     const void* fn = pick_run_batch((int)dim);
     if (int rc = set_smem(fn, L.total)) return rc;
+    A.nruns = (int)nruns;
+    A.run_order = nullptr;
+    A.run_counter = nullptr;
+    long long grid = nruns;
+    if (workers > 0) {
+        A.run_order = reinterpret_cast<const int*>(d_stage + desc_bytes);
+        A.run_counter = reinterpret_cast<unsigned*>(d_stage + desc_bytes + order_bytes);
+        grid = workers;
+    }
     void* args[] = {(void*)&A};
-    APO_CUDA(cudaLaunchKernel(fn, dim3((unsigned)nruns), dim3((unsigned)threads), args, L.total, st));
+    APO_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3((unsigned)threads), args, L.total, st));
     APO_CUDA(cudaGetLastError());
-    cudaFreeAsync(d_descs, st);
+    cudaFreeAsync(d_stage, st);
     return APO_OK;
 }
 

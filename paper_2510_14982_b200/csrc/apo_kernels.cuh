@@ -187,6 +187,11 @@ struct BatchArgs {
     int cec_bufs;   // max over the batch's objectives of cec_bufs_for(code)
     int tab_smem;   // doubles of threshold prefix table staged in shared memory (0 = none)
     int rng;        // RngMode
+    int nruns;
+    // persistent mode (run_counter non-null): CTAs claim runs run_order[0], [1], ... (costliest first) until
+    // none is left, so an SM that drew cheap runs takes more; else CTA b does run b
+    const int* run_order;
+    unsigned* run_counter;
 };
 
 struct BatchLayout {
@@ -228,11 +233,13 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
 }
 
 // MAXC >= 0: group path (apo_group.cuh); MAXC < 0: warp-per-protozoon (dim > 256).
-// Launched with kThreads when the batch fills the GPU (80 registers: 3 CTAs/SM, so the C2 suite's 360
-// runs fit one wave on 148 SMs) and with kBatchWideThreads when there are fewer runs than SMs: a run is
-// then latency-bound (one SM, ~2 warps per scheduler at 256 threads) and twice the warps halve the
-// protozoa each warp walks per iteration.
+// A run is latency-bound (one CTA walks ps protozoa per iteration behind __syncthreads), so more warps
+// per run pay: with more runs than SMs the launch is one persistent kBatchPersistThreads CTA per SM
+// that claims runs costliest first; with a handful of runs each gets a kBatchWideThreads CTA; else one
+// kThreads CTA per run (80 registers: 3 CTAs/SM).  apo_run_batch picks the shape.
 constexpr int kBatchWideThreads = 512;
+constexpr int kBatchPersistThreads = 640;
+constexpr int kBatchFewRuns = 16;
 #ifndef APO_BATCH_MAXNREG
 #define APO_BATCH_MAXNREG 80
 #endif
@@ -242,7 +249,6 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
     __shared__ unsigned long long red_min[32];
     __shared__ unsigned red_warn[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int run = blockIdx.x;
     const int ps = A.ps, dim = A.dim, ld = A.ld;
     const BatchLayout L = batch_layout(ps, dim, ld, nwarps, A.cec_bufs, A.tab_smem);
     double* pos[2] = {reinterpret_cast<double*>(smem + L.pos0), reinterpret_cast<double*>(smem + L.pos1)};
@@ -259,6 +265,17 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
     unsigned char* wbase = smem + L.warps + (size_t)warp * batch_warp_bytes(dim, A.cec_bufs);
     const GroupScratch g = group_scratch(wbase, dim, false, A.cec_bufs);
     const WarpScratch ws = MAXC >= 0 ? g.ws : warp_scratch(wbase, dim);
+    __shared__ int s_run;
+    for (int claim = 0;; claim++) {
+    if (threadIdx.x == 0) {
+        int k = A.nruns;
+        if (A.run_counter) k = (int)atomicAdd(A.run_counter, 1u);
+        else if (claim == 0) k = blockIdx.x;
+        s_run = k < A.nruns ? (A.run_order ? A.run_order[k] : k) : -1;
+    }
+    __syncthreads();
+    const int run = s_run;
+    if (run < 0) break;
     const uint64_t seed = A.seeds[run];
     ObjDesc O = A.objs[run];
     if (A.tab_smem > 0 && (O.code == OBJ_OTSU_ML || O.code == OBJ_KAPUR_ML)) {
@@ -429,6 +446,8 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
         }
     if (A.final_fit)
         for (int r = threadIdx.x; r < ps; r += blockDim.x) A.final_fit[(size_t)run * ps + r] = fit[cur][order[r]];
+    __syncthreads();  // shared memory is reused by the next claimed run
+    }
 }
 
 

@@ -221,6 +221,26 @@ def test_batch_matches_oracle_runs(pz):
     assert np.array_equal(res.best_fitness, want)
 
 
+def test_persistent_batch_matches_oracle_runs(pz):
+    """More runs than SMs: persistent CTAs claim runs costliest first (mixed objectives, so the claim
+    order is not the run order); every result must land at its own index, bit-exact."""
+    names = ["rosenbrock", "sphere", "hgbat", "bent_cigar", "high_conditioned_elliptic"] * 64
+    seeds = [7 * k + 1 for k in range(len(names))]
+    cfg = pz.ApoConfig(ps=24, dim=6, bounds=pz.Bounds(-30.0, 30.0, 6), max_iterations=40)
+    res = pz.run_batch(cfg, names, seeds, want_trace=True)
+    want, _ = oracle.run_many(names, seeds, ps=24, dim=6, max_iterations=40, lower=-30.0, upper=30.0)
+    assert np.array_equal(res.best_fitness, want)
+    assert np.array_equal(res.trace[:, -1], want)
+    # CEC2022 mixes (cost-ordered claims across functions) agree with one-run-per-CTA launches
+    cnames = [f"cec2022_f{k}" for k in range(1, 13)] * 15
+    ccfg = pz.ApoConfig(ps=30, dim=10, bounds=pz.Bounds(-100.0, 100.0, 10), max_iterations=30)
+    big = pz.run_batch(ccfg, cnames, list(range(len(cnames))))
+    for k0 in range(0, len(cnames), 12):
+        part = pz.run_batch(ccfg, cnames[k0:k0 + 12], list(range(k0, k0 + 12)))
+        assert np.array_equal(part.best_fitness, big.best_fitness[k0:k0 + 12])
+        assert np.array_equal(part.trace, big.trace[k0:k0 + 12])
+
+
 def test_histogram_and_threshold(pz):
     g = np.load(os.path.join(GOLDEN, "threshold.npz"))
     img = pz.GrayImage(g["pixels"])
