@@ -395,8 +395,10 @@ def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_t
     dev = _dev()
     n_iters = cfg.iterations_within_budget()
     descs = (_lib.apo_objective * n)()
+    dobjs = {}
     for k, o in enumerate(objs):
-        descs[k] = device_objective(o, cfg.dim).struct
+        d = dobjs.setdefault(id(o), device_objective(o, cfg.dim))
+        descs[k] = d.struct
     seeds_t = torch.as_tensor(np.array([int(s) for s in seeds], dtype=np.uint64).view(np.int64), device=dev)
     sched = torch.as_tensor(np.array(schedule_table(cfg.max_iterations))
                             if cfg.max_iterations else np.zeros(3), device=dev)
@@ -413,6 +415,9 @@ def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_t
         stream.wait_stream(torch.cuda.current_stream())
         for t in (seeds_t, sched, pdr, best_fit, best_pos, trace, fpos, ffit, warn):
             if t is not None:
+                t.record_stream(stream)
+        for d in dobjs.values():  # an Objective's tables may be freed while the kernel still reads them
+            for t in d.keep:
                 t.record_stream(stream)
     t0 = time.perf_counter()
     _lib.check(lib.apo_run_batch(n, _lib.ptr(seeds_t), descs, cfg.ps, cfg.dim, cfg.max_iterations, n_iters,

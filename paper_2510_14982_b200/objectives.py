@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass, field
+import weakref
 from functools import lru_cache
 from typing import Any, Callable, Optional
 
@@ -157,7 +158,7 @@ class DeviceObjective:
 
         if obj.code == EXTERNAL:
             raise ValueError("external objective functions cannot run on the cuda backend")
-        self.obj = obj
+        self.obj_ref = weakref.ref(obj)  # the cache must not keep its key's Objective alive
         self.dim = dim
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.keep = []
@@ -219,10 +220,13 @@ def device_objective(obj: Objective, dim: int) -> DeviceObjective:
 
     key = (id(obj), obj.name, obj.code, dim, torch.cuda.current_device())
     hit = _DEV_CACHE.get(key)
-    if hit is not None and hit.obj is obj:
+    if hit is not None and hit.obj_ref() is obj:
         return hit
     d = DeviceObjective(obj, dim)
     _DEV_CACHE[key] = d
+    # the entry (and its device tables) goes when the Objective does: per-call objectives such as the
+    # threshold ones would otherwise accumulate
+    weakref.finalize(obj, _DEV_CACHE.pop, key, None)
     return d
 
 

@@ -241,6 +241,23 @@ def test_persistent_batch_matches_oracle_runs(pz):
         assert np.array_equal(part.trace, big.trace[k0:k0 + 12])
 
 
+def test_device_objective_cache_follows_objective_lifetime(pz):
+    import copy
+    import gc
+
+    from paper_2510_14982_b200 import objectives
+
+    assert pz.get_objective("cec2022_f5") is pz.get_objective("cec2022_f5")  # interned: tables built once
+    base = len(objectives._DEV_CACHE)
+    tmp = [copy.copy(pz.get_objective("high_conditioned_elliptic")) for _ in range(5)]
+    for o in tmp:
+        objectives.device_objective(o, 7)
+    assert len(objectives._DEV_CACHE) == base + 5
+    del tmp, o
+    gc.collect()
+    assert len(objectives._DEV_CACHE) == base
+
+
 def test_histogram_and_threshold(pz):
     g = np.load(os.path.join(GOLDEN, "threshold.npz"))
     img = pz.GrayImage(g["pixels"])
