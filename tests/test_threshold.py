@@ -208,3 +208,50 @@ def test_max_threshold_count_matches_oracle():
         got = pz.evaluate_batch(obj, x)
         want = np.array([oracle.threshold_eval(method, r, obj.table) for r in x])
         np.testing.assert_allclose(got, want, rtol=KAPUR_RTOL)
+
+
+@pytest.mark.gpu
+def test_persistent_batch_mixed_tables_match_oracle():
+    """More runs than SMs (persistent CTAs, costliest-first claims) with two different prefix tables:
+    each claimed run re-stages its own table in shared memory."""
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200 import imaging
+
+    counts = np.bincount(synthetic_image(256).ravel(), minlength=256)
+    objs = {m: imaging.multilevel_objective(counts, 3, m) for m in ("otsu", "kapur")}
+    methods = ["otsu", "kapur"] * 90
+    seeds = list(range(len(methods)))
+    cfg = pz.ApoConfig(ps=30, dim=3, bounds=pz.Bounds(0.0, 255.0, 3), max_iterations=30)
+    res = pz.run_batch(cfg, [objs[m] for m in methods], seeds, want_trace=False)
+    for m in ("otsu", "kapur"):
+        idx = [i for i, x in enumerate(methods) if x == m]
+        want, _ = oracle.run_many([f"{m}_ml"] * len(idx), [seeds[i] for i in idx], ps=30, dim=3,
+                                  max_iterations=30, lower=0.0, upper=255.0, tables=[objs[m].table] * len(idx))
+        if m == "otsu":
+            assert np.array_equal(res.best_fitness[idx], want)
+        else:
+            np.testing.assert_allclose(res.best_fitness[idx], want, rtol=1e-9)
+
+
+@pytest.mark.gpu
+def test_side_stream_batch_with_a_dropped_objective():
+    """The objective (and so its cached device table) is dropped while the kernel runs on a side stream."""
+    import gc
+
+    import torch
+
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200 import imaging
+
+    counts = np.bincount(synthetic_image(256).ravel(), minlength=256)
+    cfg = pz.ApoConfig(ps=64, dim=4, bounds=pz.Bounds(0.0, 255.0, 4), max_iterations=300)
+    want = pz.run_batch(cfg, [imaging.multilevel_objective(counts, 4, "otsu")] * 8, list(range(8)),
+                        want_trace=False).best_fitness
+    st = torch.cuda.Stream()
+    out = pz.run_batch(cfg, [imaging.multilevel_objective(counts, 4, "otsu")] * 8, list(range(8)),
+                       want_trace=False, device_out=True, stream=st)
+    gc.collect()
+    junk = [torch.full((4096,), -1.0e300, dtype=torch.float64, device="cuda") for _ in range(64)]  # reuse bait
+    torch.cuda.synchronize()
+    del junk
+    assert np.array_equal(out.best_fitness.cpu().numpy(), want)
