@@ -522,14 +522,15 @@ def bench_c3():
             jobs.append((method, k, obj, cfg))
     streams = [torch.cuda.Stream() for _ in jobs]
     for (m, k, obj, cfg), st in zip(jobs, streams):  # warm-up (compiles nothing; first-launch costs)
-        pz.run_batch(cfg, [obj] * 2, [0, 1], want_trace=False, device_out=True, stream=st)
+        pz.run_batch(cfg, [obj] * 2, [0, 1], want_trace=False, device_out=True, stream=st, threads_per_run=256)
     torch.cuda.synchronize()
     e0.record()
     cur = torch.cuda.current_stream()
     outs = []
     for (m, k, obj, cfg), st in zip(jobs, streams):
         st.wait_stream(cur)
-        outs.append(pz.run_batch(cfg, [obj] * 30, list(range(30)), want_trace=False, device_out=True, stream=st))
+        outs.append(pz.run_batch(cfg, [obj] * 30, list(range(30)), want_trace=False, device_out=True, stream=st,
+                                 threads_per_run=256))
     for st in streams:
         cur.wait_stream(st)
     e1.record()

@@ -53,7 +53,26 @@ int fail(int code, const std::string& msg) {
     } while (0)
 
 
-inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+// Scratch from cudaMallocAsync stays in the device's stream-ordered pool once freed: with the default
+// release threshold (0) every synchronisation hands it back and the next step re-maps it, which at the
+// C4 shape cost 50-100 ms spikes in step() (tools/e2e_probe.py).
+void keep_mempool() {
+    static const bool done = [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        return true;
+    }();
+    (void)done;
+}
+
+inline cudaStream_t as_stream(void* s) {
+    keep_mempool();
+    return reinterpret_cast<cudaStream_t>(s);
+}
 
 int num_sms() {
     static int n = 0;
@@ -1354,7 +1373,19 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
                   double upper, double eps, const double* sched, const double* p_dr, double* best_fit,
                   double* best_pos, double* trace, double* final_pos, double* final_fit, int64_t* warnings,
                   int rng, void* stream) {
+    return apo_run_batch_shaped(nruns, seeds, objectives_host, ps, dim, max_iterations, n_iters, npairs, pf_max,
+                                lower, upper, eps, sched, p_dr, best_fit, best_pos, trace, final_pos, final_fit,
+                                warnings, rng, 0, stream);
+}
+
+int apo_run_batch_shaped(int64_t nruns, const uint64_t* seeds, const apo_objective* objectives_host, int64_t ps,
+                         int64_t dim, int64_t max_iterations, int64_t n_iters, int64_t npairs, double pf_max,
+                         double lower, double upper, double eps, const double* sched, const double* p_dr,
+                         double* best_fit, double* best_pos, double* trace, double* final_pos, double* final_fit,
+                         int64_t* warnings, int rng, int threads_per_run, void* stream) {
     APO_CHECK(rng == RNG_KEYED || rng == RNG_PHILOX, "rng must be APO_RNG_KEYED or APO_RNG_PHILOX");
+    APO_CHECK(threads_per_run == 0 || (threads_per_run >= 32 && threads_per_run <= 1024 && threads_per_run % 32 == 0),
+              "threads_per_run must be 0 or a multiple of 32 in [32, 1024]");
     APO_CHECK(nruns >= 1 && nruns < (1LL << 31), "nruns out of range");
     APO_CHECK(ps >= 1 && dim >= 1 && dim <= 8192, "bad shape");
     APO_CHECK(n_iters >= 0 && n_iters <= max_iterations, "n_iters must be in [0, max_iterations]");
@@ -1415,10 +1446,10 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs, A.tab_smem);
     APO_CHECK((int64_t)L.total + 2048 <= smem_optin(), "population too large for the shared-memory batch kernel");
     // Launch shape (k_run_batch's comment): more runs than SMs -> one persistent kBatchPersistThreads CTA
-    // per SM claiming runs costliest first (C2: 360 runs 1.6x faster than 3 x 256-thread CTAs per SM with
-    // one run each, whose slowest SM holds three heavy runs); a handful of runs -> one wide CTA each
-    // (latency-bound); in between -> one 256-thread CTA per run, 3 per SM, which leaves room for batches
-    // launched concurrently on other streams.  APO_BATCH_THREADS / APO_BATCH_WORKERS override (A/B runs).
+    // per SM claiming runs costliest first (C2: 360 runs 1.8x faster than 3 x 256-thread CTAs per SM
+    // with one run each, whose slowest SM holds three heavy runs); else one kBatchWideThreads CTA per
+    // run (a run is latency-bound).  threads_per_run > 0 forces one CTA of that size per run (batches
+    // sharing the GPU with others).  APO_BATCH_THREADS / APO_BATCH_WORKERS override (A/B runs).
     static const int env_threads = getenv("APO_BATCH_THREADS") ? atoi(getenv("APO_BATCH_THREADS")) : 0;
     static const int env_workers = getenv("APO_BATCH_WORKERS") ? atoi(getenv("APO_BATCH_WORKERS")) : 0;
     const int sms = num_sms();
@@ -1427,10 +1458,12 @@ int apo_run_batch(int64_t nruns, const uint64_t* seeds, const apo_objective* obj
     if (env_threads > 0 || env_workers > 0) {
         if (env_threads > 0) threads = env_threads & ~31;
         if (env_workers > 0 && env_workers < nruns) workers = env_workers;
+    } else if (threads_per_run > 0) {
+        threads = threads_per_run;
     } else if (nruns > sms) {
         threads = kBatchPersistThreads;
         workers = sms;
-    } else if (nruns <= kBatchFewRuns && ps > (int64_t)kWarps) {
+    } else if (ps > (int64_t)kWarps) {
         threads = kBatchWideThreads;
     }
     APO_CHECK(threads >= 32 && threads <= 1024, "APO_BATCH_THREADS must be in [32, 1024]");

@@ -235,11 +235,10 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
 // MAXC >= 0: group path (apo_group.cuh); MAXC < 0: warp-per-protozoon (dim > 256).
 // A run is latency-bound (one CTA walks ps protozoa per iteration behind __syncthreads), so more warps
 // per run pay: with more runs than SMs the launch is one persistent kBatchPersistThreads CTA per SM
-// that claims runs costliest first; with a handful of runs each gets a kBatchWideThreads CTA; else one
-// kThreads CTA per run (80 registers: 3 CTAs/SM).  apo_run_batch picks the shape.
+// that claims runs costliest first, else each run gets a kBatchWideThreads CTA; callers sharing the GPU
+// can ask for kThreads CTAs (80 registers: 3 CTAs/SM).  apo_run_batch_shaped picks the shape.
 constexpr int kBatchWideThreads = 512;
 constexpr int kBatchPersistThreads = 640;
-constexpr int kBatchFewRuns = 16;
 #ifndef APO_BATCH_MAXNREG
 #define APO_BATCH_MAXNREG 80
 #endif

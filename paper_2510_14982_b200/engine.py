@@ -379,8 +379,12 @@ class BatchResult:
 
 
 def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_trace: bool = True,
-              want_population: bool = False, device_out: bool = False, stream=None) -> BatchResult:
-    """Independent runs (same ps/dim/bounds/T), one CTA each, on the current GPU."""
+              want_population: bool = False, device_out: bool = False, stream=None,
+              threads_per_run: int = 0) -> BatchResult:
+    """Independent runs (same ps/dim/bounds/T), each resident in one CTA's shared memory, on the current GPU.
+
+    threads_per_run = 0 lets the library pick the launch shape (apo_run_batch_shaped); pass 256 when
+    several batches run concurrently on different streams so their CTAs share the SMs."""
     import torch
 
     lib = _lib.require_cuda()
@@ -420,11 +424,12 @@ def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_t
             for t in d.keep:
                 t.record_stream(stream)
     t0 = time.perf_counter()
-    _lib.check(lib.apo_run_batch(n, _lib.ptr(seeds_t), descs, cfg.ps, cfg.dim, cfg.max_iterations, n_iters,
-                                 cfg.neighbor_pairs, cfg.pf_max, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,
-                                 _lib.ptr(sched), _lib.ptr(pdr), _lib.ptr(best_fit), _lib.ptr(best_pos),
-                                 _lib.ptr(trace), _lib.ptr(fpos), _lib.ptr(ffit), _lib.ptr(warn),
-                                 rng_code(cfg), _lib.stream_handle(stream)), "apo_run_batch")
+    _lib.check(lib.apo_run_batch_shaped(n, _lib.ptr(seeds_t), descs, cfg.ps, cfg.dim, cfg.max_iterations, n_iters,
+                                        cfg.neighbor_pairs, cfg.pf_max, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,
+                                        _lib.ptr(sched), _lib.ptr(pdr), _lib.ptr(best_fit), _lib.ptr(best_pos),
+                                        _lib.ptr(trace), _lib.ptr(fpos), _lib.ptr(ffit), _lib.ptr(warn),
+                                        rng_code(cfg), int(threads_per_run), _lib.stream_handle(stream)),
+               "apo_run_batch_shaped")
     if device_out:
         return BatchResult(best_fit, best_pos, trace, warn, fpos, ffit, 0.0, tuple(o.name for o in objs),
                            tuple(seeds))

@@ -189,8 +189,9 @@ def test_concurrent_stream_batches_match_sequential():
     streams = [torch.cuda.Stream() for _ in jobs]
     for (obj, cfg), st in zip(jobs, streams):  # results dropped while the kernels run
         pz.run_batch(cfg, [obj] * 6, list(range(6)), want_trace=False, device_out=True, stream=st)
-    outs = [pz.run_batch(cfg, [obj] * 6, list(range(6)), want_trace=False, device_out=True, stream=st)
-            for (obj, cfg), st in zip(jobs, streams)]
+    outs = [pz.run_batch(cfg, [obj] * 6, list(range(6)), want_trace=False, device_out=True, stream=st,
+                         threads_per_run=256 if k % 2 else 0)
+            for k, ((obj, cfg), st) in enumerate(zip(jobs, streams))]
     torch.cuda.synchronize()
     for o, s in zip(outs, seq):
         assert np.array_equal(o.best_fitness.cpu().numpy(), s)
