@@ -239,6 +239,7 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
 // can ask for kThreads CTAs (80 registers: 3 CTAs/SM).  apo_run_batch_shaped picks the shape.
 constexpr int kBatchWideThreads = 512;
 constexpr int kBatchPersistThreads = 640;
+constexpr int kBatchMaxThreads = 768;  // 80 registers x 768 threads fill the 64K register file
 #ifndef APO_BATCH_MAXNREG
 #define APO_BATCH_MAXNREG 80
 #endif

@@ -241,6 +241,22 @@ def test_persistent_batch_matches_oracle_runs(pz):
         assert np.array_equal(part.trace, big.trace[k0:k0 + 12])
 
 
+def test_batch_launch_shapes_agree(pz):
+    """apo_run_batch_shaped: any CTA size gives the same runs (rank counts, group sizes and the Dr warp
+    depend on it, the results must not); out-of-range sizes are rejected."""
+    names = [f"cec2022_f{k}" for k in (1, 6, 9, 12)] + ["rosenbrock", "griewank"]
+    seeds = list(range(len(names)))
+    cfg = pz.ApoConfig(ps=70, dim=12, bounds=pz.Bounds(-100.0, 100.0, 12), max_iterations=60)
+    ref = pz.run_batch(cfg, names, seeds)
+    for threads in (64, 256, 384, 768):
+        got = pz.run_batch(cfg, names, seeds, threads_per_run=threads)
+        assert np.array_equal(got.trace, ref.trace), threads
+        assert np.array_equal(got.best_position, ref.best_position), threads
+    for bad in (16, 1024, 100):
+        with pytest.raises(Exception, match="threads_per_run"):
+            pz.run_batch(cfg, names, seeds, threads_per_run=bad)
+
+
 def test_device_objective_cache_follows_objective_lifetime(pz):
     import copy
     import gc
