@@ -235,6 +235,9 @@ int apo_run_batch_shaped(int64_t nruns, const uint64_t *seeds, const apo_objecti
                          double lower, double upper, double eps, const double *sched, const double *p_dr,
                          double *best_fit, double *best_pos, double *trace, double *final_pos, double *final_fit,
                          int64_t *warnings, int rng, int threads_per_run, void *stream);
+/* Device scratch and run buffers freed by the library stay in the current device's stream-ordered
+ * pool for reuse (no cudaMalloc/cudaFree per run or step); this returns them to the driver. */
+int apo_release_cached_memory(void);
 /* Largest ps*dim the batch kernel can hold in shared memory (basic objectives). */
 int64_t apo_run_batch_max_elems(int64_t ps, int64_t dim);
 /* 1 if a batch of these objectives at (ps, dim) fits the shared-memory batch kernel. */

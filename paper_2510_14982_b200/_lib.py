@@ -145,6 +145,7 @@ PROTOTYPES = {
     "apo_run_batch_shaped": (_INT, [_I, _P, C.POINTER(apo_objective), _I, _I, _I, _I, _I, _D, _D, _D, _D, _P, _P,
                                     _P, _P, _P, _P, _P, _P, _INT, _INT, _P]),
     "apo_run_batch_max_elems": (_I, [_I, _I]),
+    "apo_release_cached_memory": (_INT, []),
     "apo_run_batch_fits": (_INT, [_I, _I, C.POINTER(apo_objective), _I]),
     "apo_shard_create": (_INT, [C.POINTER(C.c_void_p), _I, _I, _I, _I, _U, _I, _D, _D, _D, _D,
                                 C.POINTER(apo_objective), _P, _P, _INT, _P, _P, _P, _P, _P]),

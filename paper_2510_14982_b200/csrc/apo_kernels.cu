@@ -830,8 +830,10 @@ int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iteration
     const size_t tb_dr = dr_tmp_bytes(r->dr_cap, ps);
     r->tmp_bytes = tb_sort > tb_dr ? tb_sort : tb_dr;
     cudaError_t e = cudaSuccess;
+    // stream-ordered allocations: the pool keeps them after apo_run_destroy (keep_mempool), so creating
+    // and destroying runs costs no cudaMalloc/cudaFree (hundreds of ms at the C4 shape)
     auto alloc = [&](void** p, size_t b) {
-        if (e == cudaSuccess) e = cudaMalloc(p, b > 0 ? b : 16);
+        if (e == cudaSuccess) e = cudaMallocAsync(p, b > 0 ? b : 16, st);
     };
     alloc((void**)&r->pos[0], rows);
     alloc((void**)&r->pos[1], rows);
@@ -1117,8 +1119,18 @@ int apo_run_destroy(apo_run* r) {
                     r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn, r->cand_ok,
                     r->tile_counter};
     for (void* b : bufs)
-        if (b) cudaFree(b);
+        if (b) cudaFreeAsync(b, r->stream);
     delete r;
+    return APO_OK;
+}
+
+int apo_release_cached_memory(void) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    APO_CUDA(cudaGetDevice(&dev));
+    APO_CUDA(cudaDeviceSynchronize());
+    APO_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    APO_CUDA(cudaMemPoolTrimTo(pool, 0));
     return APO_OK;
 }
 

@@ -324,3 +324,19 @@ def test_random_configurations_bit_exact(pz, c, monkeypatch):
         assert np.array_equal(res.population.positions, want["positions"])
         assert np.array_equal(res.population.fitness, want["fitness"])
         assert res.warnings == want["warnings"] and res.best_fitness == want["best_fitness"]
+
+
+def test_run_buffers_recycled_and_released(pz):
+    """Run buffers come from the stream-ordered pool: create/destroy repeatedly, populations stay
+    right, and empty_cache() hands the pool back."""
+    import torch
+
+    cfg = pz.ApoConfig(ps=5000, dim=30, bounds=pz.Bounds(-100.0, 100.0, 30), max_iterations=5, seed=4)
+    first = pz.run(cfg, "cec2022_f4")
+    for _ in range(3):
+        again = pz.run(cfg, "cec2022_f4")
+        assert np.array_equal(again.population.positions, first.population.positions)
+        assert np.array_equal(again.trace, first.trace)
+    pz.empty_cache()
+    torch.cuda.synchronize()
+    assert np.array_equal(pz.run(cfg, "cec2022_f4").population.fitness, first.population.fitness)
