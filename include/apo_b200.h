@@ -228,7 +228,7 @@ int apo_run_batch(int64_t nruns, const uint64_t *seeds, const apo_objective *obj
                   int rng, void *stream);
 /* apo_run_batch with an explicit CTA size: threads_per_run = 0 picks the shape (more runs than SMs:
  * one persistent 640-thread CTA per SM claiming runs costliest first; else one 512-thread CTA per
- * run); a multiple of 32 in [32, 768] forces one CTA of that many threads per run -- e.g. 256 when several batches run
+ * run); a multiple of 32 in [32, 640] forces one CTA of that many threads per run -- e.g. 256 when several batches run
  * concurrently on different streams and must share the SMs. */
 int apo_run_batch_shaped(int64_t nruns, const uint64_t *seeds, const apo_objective *objectives_host, int64_t ps,
                          int64_t dim, int64_t max_iterations, int64_t n_iters, int64_t npairs, double pf_max,

@@ -1398,7 +1398,7 @@ int apo_run_batch_shaped(int64_t nruns, const uint64_t* seeds, const apo_objecti
     APO_CHECK(rng == RNG_KEYED || rng == RNG_PHILOX, "rng must be APO_RNG_KEYED or APO_RNG_PHILOX");
     APO_CHECK(threads_per_run == 0 || (threads_per_run >= 32 && threads_per_run <= kBatchMaxThreads &&
                                        threads_per_run % 32 == 0),
-              "threads_per_run must be 0 or a multiple of 32 in [32, 768]");
+              "threads_per_run must be 0 or a multiple of 32 in [32, 640]");
     APO_CHECK(nruns >= 1 && nruns < (1LL << 31), "nruns out of range");
     APO_CHECK(ps >= 1 && dim >= 1 && dim <= 8192, "bad shape");
     APO_CHECK(n_iters >= 0 && n_iters <= max_iterations, "n_iters must be in [0, max_iterations]");
@@ -1479,7 +1479,7 @@ int apo_run_batch_shaped(int64_t nruns, const uint64_t* seeds, const apo_objecti
     } else if (ps > (int64_t)kWarps) {
         threads = kBatchWideThreads;
     }
-    APO_CHECK(threads >= 32 && threads <= kBatchMaxThreads, "APO_BATCH_THREADS must be in [32, 768]");
+    APO_CHECK(threads >= 32 && threads <= kBatchMaxThreads, "APO_BATCH_THREADS must be in [32, 640]");
     if (threads != kThreads) {
         const BatchLayout W = batch_layout(A.ps, A.dim, A.ld, threads / 32, A.cec_bufs, A.tab_smem);
         if ((int64_t)W.total + 2048 <= smem_optin()) {

@@ -236,12 +236,12 @@ __host__ __device__ inline BatchLayout batch_layout(int ps, int dim, int ld, int
 // A run is latency-bound (one CTA walks ps protozoa per iteration behind __syncthreads), so more warps
 // per run pay: with more runs than SMs the launch is one persistent kBatchPersistThreads CTA per SM
 // that claims runs costliest first, else each run gets a kBatchWideThreads CTA; callers sharing the GPU
-// can ask for kThreads CTAs (80 registers: 3 CTAs/SM).  apo_run_batch_shaped picks the shape.
+// can ask for kThreads CTAs (96 registers: 2 CTAs/SM).  apo_run_batch_shaped picks the shape.
 constexpr int kBatchWideThreads = 512;
 constexpr int kBatchPersistThreads = 640;
-constexpr int kBatchMaxThreads = 768;  // 80 registers x 768 threads fill the 64K register file
+constexpr int kBatchMaxThreads = 640;  // 96 registers: 5 warps per SM sub-partition (16K registers each)
 #ifndef APO_BATCH_MAXNREG
-#define APO_BATCH_MAXNREG 80
+#define APO_BATCH_MAXNREG 96
 #endif
 template <int MAXC>
 __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {

@@ -248,11 +248,11 @@ def test_batch_launch_shapes_agree(pz):
     seeds = list(range(len(names)))
     cfg = pz.ApoConfig(ps=70, dim=12, bounds=pz.Bounds(-100.0, 100.0, 12), max_iterations=60)
     ref = pz.run_batch(cfg, names, seeds)
-    for threads in (64, 256, 384, 768):
+    for threads in (64, 256, 384, 640):
         got = pz.run_batch(cfg, names, seeds, threads_per_run=threads)
         assert np.array_equal(got.trace, ref.trace), threads
         assert np.array_equal(got.best_position, ref.best_position), threads
-    for bad in (16, 1024, 100):
+    for bad in (16, 672, 1024, 100):
         with pytest.raises(Exception, match="threads_per_run"):
             pz.run_batch(cfg, names, seeds, threads_per_run=bad)
 
