@@ -490,7 +490,7 @@ def bench_c1():
     return out
 
 
-def bench_c3():
+def bench_c3(threads_per_run=320):
     """BASELINE config 3: multilevel Otsu and Kapur (k = 2..5 thresholds) on a synthetic 4096x4096 8-bit
     image; ps=100, T=1000, 30 seeds per (method, k), the 8 batches on 8 concurrent streams."""
     import torch
@@ -522,7 +522,8 @@ def bench_c3():
             jobs.append((method, k, obj, cfg))
     streams = [torch.cuda.Stream() for _ in jobs]
     for (m, k, obj, cfg), st in zip(jobs, streams):  # warm-up (compiles nothing; first-launch costs)
-        pz.run_batch(cfg, [obj] * 2, [0, 1], want_trace=False, device_out=True, stream=st, threads_per_run=256)
+        pz.run_batch(cfg, [obj] * 2, [0, 1], want_trace=False, device_out=True, stream=st,
+                     threads_per_run=threads_per_run)
     torch.cuda.synchronize()
     e0.record()
     cur = torch.cuda.current_stream()
@@ -530,7 +531,7 @@ def bench_c3():
     for (m, k, obj, cfg), st in zip(jobs, streams):
         st.wait_stream(cur)
         outs.append(pz.run_batch(cfg, [obj] * 30, list(range(30)), want_trace=False, device_out=True, stream=st,
-                                 threads_per_run=256))
+                                 threads_per_run=threads_per_run))
     for st in streams:
         cur.wait_stream(st)
     e1.record()
