@@ -112,6 +112,16 @@ int apo_run_updates_obj(const double *positions, const double *fitness, const ui
                         uint64_t key_iteration, int64_t npairs, double lower, double upper, double eps, double p_ah,
                         double f_mult, double decay, const apo_objective *objective_host, const double *p_dr,
                         unsigned long long *warn_count, void *stream);
+/* apo_run_updates_obj restricted to ranks [rank_lo, rank_hi) (rows of out_pos/out_fit/out_acc outside
+ * are not written; every row of positions may still be read as a partner).  warn_count is added to,
+ * not reset, so a caller can split one update into chunks -- e.g. to copy finished ranks to the host
+ * while the next chunk computes. */
+int apo_run_updates_range(const double *positions, const double *fitness, const uint8_t *in_dr, double *out_pos,
+                          double *out_fit, uint8_t *out_acc, uint8_t *out_warn, int64_t ps, int64_t dim,
+                          uint64_t seed, uint64_t key_iteration, int64_t npairs, double lower, double upper,
+                          double eps, double p_ah, double f_mult, double decay, const apo_objective *objective_host,
+                          const double *p_dr, unsigned long long *warn_count, int64_t rank_lo, int64_t rank_hi,
+                          void *stream);
 
 /* Batch fitness: out[r] = f(x[r*ld .. r*ld+dim)) (objectives.evaluate_unchecked,
  * objectives.py:222-228). */

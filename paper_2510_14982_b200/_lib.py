@@ -121,6 +121,8 @@ PROTOTYPES = {
                                _I, _P, _P, _P]),
     "apo_run_updates_obj": (_INT, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _U, _U, _I, _D, _D, _D, _D, _D, _D,
                                    C.POINTER(apo_objective), _P, _P, _P]),
+    "apo_run_updates_range": (_INT, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _U, _U, _I, _D, _D, _D, _D, _D, _D,
+                                     C.POINTER(apo_objective), _P, _P, _I, _I, _P]),
     "apo_evaluate": (_INT, [_P, _I, _I, _I, C.POINTER(apo_objective), _P, _P]),
     "apo_initialize": (_INT, [_U, _I, _I, _I, _D, _D, C.POINTER(apo_objective), _P, _P, _P]),
     "apo_sort_order": (_INT, [_P, _I, _P, _P]),

@@ -592,7 +592,20 @@ int apo_run_updates_obj(const double* positions, const double* fitness, const ui
                         uint64_t key_iteration, int64_t npairs, double lower, double upper, double eps, double p_ah,
                         double f_mult, double decay, const apo_objective* objective_host, const double* p_dr,
                         unsigned long long* warn_count, void* stream) {
+    if (warn_count) APO_CUDA(cudaMemsetAsync(warn_count, 0, sizeof(unsigned long long), as_stream(stream)));
+    return apo_run_updates_range(positions, fitness, in_dr, out_pos, out_fit, out_acc, out_warn, ps, dim, seed,
+                                 key_iteration, npairs, lower, upper, eps, p_ah, f_mult, decay, objective_host, p_dr,
+                                 warn_count, 0, ps, stream);
+}
+
+int apo_run_updates_range(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
+                          double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim,
+                          uint64_t seed, uint64_t key_iteration, int64_t npairs, double lower, double upper,
+                          double eps, double p_ah, double f_mult, double decay, const apo_objective* objective_host,
+                          const double* p_dr, unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi,
+                          void* stream) {
     APO_CHECK(ps >= 1 && ps < (1LL << 31), "ps out of range");
+    APO_CHECK(0 <= rank_lo && rank_lo < rank_hi && rank_hi <= ps, "rank range must satisfy 0 <= lo < hi <= ps");
     APO_CHECK(dim >= 1 && dim <= 8192, "dim out of range (1..8192)");
     APO_CHECK(npairs >= 1, "npairs must be >= 1");
     APO_CHECK(positions && fitness && in_dr && out_pos && out_fit && p_dr, "NULL buffer");
@@ -613,9 +626,10 @@ int apo_run_updates_obj(const double* positions, const double* fitness, const ui
     P.f_mult = f_mult;
     P.decay = decay;
     P.rng = RNG_KEYED;  // the reference-facing boundary is always oracle mode
-    if (warn_count) APO_CUDA(cudaMemsetAsync(warn_count, 0, sizeof(unsigned long long), as_stream(stream)));
     UpdArgs A{};
     A.P = P;
+    A.rank_lo = (int)rank_lo;
+    A.rank_hi = (int)rank_hi;
     A.O = to_desc(objective_host);
     A.pos = positions;
     A.out_pos = out_pos;

@@ -150,6 +150,9 @@ def initialize(cfg: ApoConfig, objective) -> Population:
     return Population(hp, hf, iteration=0, fe_count=cfg.ps, warnings=0)
 
 
+STEP_CHUNK_MIN_PS = 1 << 16  # step(): overlap the result's D2H with the update from this size on
+
+
 def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: EngineMode = None,
          backend: Optional[str] = None) -> Population:
     """One full iteration; returns the next population, input untouched (engine.py:142-172)."""
@@ -178,9 +181,17 @@ def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: Engin
     in_dr = torch.empty(cfg.ps, dtype=torch.uint8, device=dev)
     _lib.check(lib.apo_select_dr(cfg.seed, iteration + 1, cfg.ps, cfg.pf_max, _lib.ptr(in_dr), None, stream),
                "apo_select_dr")
-    new_pos, new_fit, _acc, warned = bk.run_updates(snap_pos, snap_fit, in_dr, cfg, obj, iteration, iteration + 1,
-                                                    parallel=(mode.kind == PARALLEL), workers=workers)
-    hp, hf = _to_host(new_pos, new_fit)
+    if cfg.ps >= STEP_CHUNK_MIN_PS and bk.NAME == "cuda":
+        # large populations: copy finished rank chunks back while the next chunk updates
+        from .kernels import cuda_backend
+
+        hp, hf, warned = cuda_backend.run_updates_to_host(snap_pos, snap_fit, in_dr, cfg, obj, iteration,
+                                                          iteration + 1)
+    else:
+        new_pos, new_fit, _acc, warned = bk.run_updates(snap_pos, snap_fit, in_dr, cfg, obj, iteration,
+                                                        iteration + 1, parallel=(mode.kind == PARALLEL),
+                                                        workers=workers)
+        hp, hf = _to_host(new_pos, new_fit)
     return Population(hp, hf, iteration=iteration + 1, fe_count=pop.fe_count + cfg.ps,
                       warnings=pop.warnings + warned)
 

@@ -74,3 +74,43 @@ def run_updates(positions, fitness, in_dr, cfg: ApoConfig, objective: Objective,
     if host:
         return out_pos.cpu().numpy(), out_fit.cpu().numpy(), acc.cpu().numpy().astype(bool), int(warn.item())
     return out_pos, out_fit, acc.bool(), int(warn.item())
+
+
+def run_updates_to_host(pos, fit, in_dr, cfg: ApoConfig, objective: Objective, iteration: int, key_iteration: int,
+                        chunks: int = 4):
+    """run_updates on device tensors with the result delivered to page-locked host memory: the update
+    runs in rank chunks (apo_run_updates_range) and each finished chunk is copied back on a second
+    stream while the next one computes.  Returns (positions, fitness) numpy views and the warning count;
+    bit-identical to run_updates."""
+    import torch
+
+    lib = _lib.require_cuda()
+    dev = pos.device
+    ps, dim = pos.shape
+    out_pos = torch.empty_like(pos)
+    out_fit = torch.empty_like(fit)
+    warn = torch.zeros(1, dtype=torch.int64, device=dev)
+    hp = torch.empty((ps, dim), dtype=torch.float64, pin_memory=True)
+    hf = torch.empty(ps, dtype=torch.float64, pin_memory=True)
+    p_ah, f_mult, decay = iteration_scalars(iteration, cfg.max_iterations)
+    dobj = device_objective(objective, dim)
+    pdr = p_dr_device(ps, dev)
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream(device=dev)
+    step = -(-ps // chunks)
+    step = (step + 31) // 32 * 32
+    for lo in range(0, ps, step):
+        hi = min(ps, lo + step)
+        _lib.check(lib.apo_run_updates_range(
+            _lib.ptr(pos), _lib.ptr(fit), _lib.ptr(in_dr), _lib.ptr(out_pos), _lib.ptr(out_fit), None, None,
+            ps, dim, cfg.seed, key_iteration, cfg.neighbor_pairs, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,
+            p_ah, f_mult, decay, dobj.ref, _lib.ptr(pdr), _lib.ptr(warn), lo, hi, _lib.stream_handle()),
+            "apo_run_updates_range")
+        copy.wait_stream(compute)
+        with torch.cuda.stream(copy):
+            hp[lo:hi].copy_(out_pos[lo:hi], non_blocking=True)
+            hf[lo:hi].copy_(out_fit[lo:hi], non_blocking=True)
+    for t in (out_pos, out_fit):
+        t.record_stream(copy)
+    copy.synchronize()
+    return hp.numpy(), hf.numpy(), int(warn.item())

@@ -340,3 +340,20 @@ def test_run_buffers_recycled_and_released(pz):
     pz.empty_cache()
     torch.cuda.synchronize()
     assert np.array_equal(pz.run(cfg, "cec2022_f4").population.fitness, first.population.fitness)
+
+
+@pytest.mark.parametrize("name,dim", [("rosenbrock", 20), ("cec2022_f6", 40), ("cec2022_f1", 150), ("griewank", 300)])
+def test_step_chunked_d2h_matches_single_launch(pz, name, dim, monkeypatch):
+    """step() at ps >= 2^16 updates in rank chunks (apo_run_updates_range) and copies each back while the
+    next computes; identical to the one-launch update, for the group, CEC split, CEC GEMM and warp paths."""
+    from paper_2510_14982_b200 import engine
+
+    cfg = pz.ApoConfig(ps=70_001, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=10, seed=9,
+                       pf_max=0.3)
+    pop = pz.initialize(cfg, name)
+    chunked = pz.step(pop, cfg, name, 3)
+    monkeypatch.setattr(engine, "STEP_CHUNK_MIN_PS", 1 << 40)
+    whole = pz.step(pop, cfg, name, 3)
+    assert np.array_equal(chunked.positions, whole.positions)
+    assert np.array_equal(chunked.fitness, whole.fitness)
+    assert chunked.warnings == whole.warnings
