@@ -27,6 +27,9 @@ for name, ps, dim in [("rosenbrock", 300, 37), ("cec2022_f6", 700, 50), ("cec202
 for ps in (3000, 30000):                   # tile sort + merge prologue, CUB prologue (device loop)
     engine.BATCH_PS_LIMIT = 0
     pz.run(pz.ApoConfig(ps=ps, dim=5, bounds=pz.Bounds(-5.0, 5.0, 5), max_iterations=3, seed=2, pf_max=1.0), "sphere")
+ccfg = pz.ApoConfig(ps=70_000, dim=5, bounds=pz.Bounds(-5.0, 5.0, 5), max_iterations=3, seed=1)
+for name in ("rosenbrock", "cec2022_f4"):                   # step(): rank-chunked update + overlapped D2H
+    pz.step(pz.initialize(ccfg, name), ccfg, name, 0)
 scfg = pz.ApoConfig(ps=16, dim=10, bounds=pz.Bounds(-5.0, 5.0, 10), max_iterations=3)
 pz.run_batch(scfg, ["cec2022_f12", "sphere", "cec2022_f7"] * 60, list(range(180)))  # persistent claims
 pz.run_batch(scfg, ["cec2022_f1"] * 4, list(range(4)), threads_per_run=64)        # explicit CTA size
