@@ -361,7 +361,8 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         long long G = env_g > 0 ? env_g : (ranks + slots - 1) / slots;
         a.gsize = (int)(G < 1 ? 1 : G > 32 ? 32 : G);
     }
-    const long long units = group ? ((long long)(a.rank_hi - a.rank_lo) + a.gsize - 1) / a.gsize : (long long)a.P.ps;
+    const long long units = group ? ((long long)(a.rank_hi - a.rank_lo) + a.gsize - 1) / a.gsize
+                                  : (long long)(a.rank_hi - a.rank_lo);
     const long long need = (units + w - 1) / w;
     const int grid = (int)(need < cap ? need : cap);
     {

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kThreads) k_update(UpdArgs A) {
     const WarpScratch s = warp_scratch(smem + (size_t)warp * warp_scratch_bytes(P.dim), P.dim);
     unsigned long long my_min = ~0ull;
     unsigned my_warn = 0;
-    for (int r0 = blockIdx.x * nwarps + warp; r0 < P.ps; r0 += gridDim.x * nwarps) {
+    for (int r0 = A.rank_lo + blockIdx.x * nwarps + warp; r0 < A.rank_hi; r0 += gridDim.x * nwarps) {
         const bool dr = A.in_dr_bits ? ((A.in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0 : A.in_dr_bytes[r0] != 0;
         const double pdr = dr ? A.p_dr[r0] : 0.0;
         UpdateResult res;

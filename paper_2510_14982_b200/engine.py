@@ -447,6 +447,9 @@ def run_batch(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_t
         return BatchResult(best_fit, best_pos, trace, warn, fpos, ffit, 0.0, tuple(o.name for o in objs),
                            tuple(seeds))
 
+    if stream is not None:  # the host copies below run on the current stream: order them after the kernel
+        torch.cuda.current_stream().wait_stream(stream)
+
     def host(t):
         return None if t is None else t.cpu().numpy()
 
@@ -463,22 +466,24 @@ def empty_cache() -> None:
 
 
 def run_many(cfg: ApoConfig, objectives: Sequence, seeds: Sequence[int], want_trace: bool = False,
-             group=None) -> BatchResult:
+             group=None, batch_fn=None) -> BatchResult:
     """Seeds x objectives sharded across the ranks of torch.distributed (if initialised).
 
     Run k goes to rank k % world_size; there is no collective while runs
     execute -- one all-gather of the per-run results at the end.  Results
     are identical for any world size (every draw is keyed by seed, not by
-    placement).
+    placement).  ``batch_fn`` (default ``run_batch``) runs this rank's share; the CPU tests pass an
+    oracle stand-in to exercise the sharding and the gather without a device.
     """
     import torch
     import torch.distributed as dist
 
+    batch_fn = batch_fn or run_batch
     objs = [resolve_objective(o) for o in objectives]
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
     mine = list(range(rank, len(objs), world))
-    local = run_batch(cfg, [objs[k] for k in mine], [seeds[k] for k in mine], want_trace=want_trace) if mine else None
+    local = batch_fn(cfg, [objs[k] for k in mine], [seeds[k] for k in mine], want_trace=want_trace) if mine else None
     if world == 1:
         return local
     n_iters = cfg.iterations_within_budget()

@@ -169,7 +169,8 @@ class DeviceObjective:
             table = obj.table
         self.struct = _lib.apo_objective()
         self.struct.code = int(obj.code)
-        if obj.data is not None and hasattr(obj.data, "arrays"):  # CEC2022
+        data = getattr(obj, "data", None)  # the reference's Objective has no CEC2022 data
+        if data is not None and hasattr(data, "arrays"):  # CEC2022
             shift, rot, shuffle = obj.data.arrays(dim)
             rot_t = np.ascontiguousarray(np.transpose(rot, (0, 2, 1)))
             arrays = [("shift", shift), ("rot_t", rot_t), ("shuffle", shuffle)]

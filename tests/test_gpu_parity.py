@@ -342,13 +342,18 @@ def test_run_buffers_recycled_and_released(pz):
     assert np.array_equal(pz.run(cfg, "cec2022_f4").population.fitness, first.population.fitness)
 
 
-@pytest.mark.parametrize("name,dim", [("rosenbrock", 20), ("cec2022_f6", 40), ("cec2022_f1", 150), ("griewank", 300)])
-def test_step_chunked_d2h_matches_single_launch(pz, name, dim, monkeypatch):
+@pytest.mark.parametrize("name,dim,bound", [("rosenbrock", 20, 100.0), ("cec2022_f6", 40, 100.0),
+                                            ("cec2022_f1", 150, 100.0), ("griewank", 300, 100.0),
+                                            ("cec2022_f1", 300, 100.0), ("sphere", 300, 1e200)])
+def test_step_chunked_d2h_matches_single_launch(pz, name, dim, bound, monkeypatch):
     """step() at ps >= 2^16 updates in rank chunks (apo_run_updates_range) and copies each back while the
-    next computes; identical to the one-launch update, for the group, CEC split, CEC GEMM and warp paths."""
+    next computes; identical to the one-launch update, for the group, CEC split, CEC GEMM and warp paths.
+    The warp path (D > 256) must honour the rank range: F1 at D=300 is the GEMM path whose candidate rows
+    would be overwritten by a later chunk, and sphere at +-1e200 overflows to inf, so every candidate
+    warns and a chunk that re-ran the whole population would over-count."""
     from paper_2510_14982_b200 import engine
 
-    cfg = pz.ApoConfig(ps=70_001, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=10, seed=9,
+    cfg = pz.ApoConfig(ps=70_001, dim=dim, bounds=pz.Bounds(-bound, bound, dim), max_iterations=10, seed=9,
                        pf_max=0.3)
     pop = pz.initialize(cfg, name)
     chunked = pz.step(pop, cfg, name, 3)
@@ -357,3 +362,5 @@ def test_step_chunked_d2h_matches_single_launch(pz, name, dim, monkeypatch):
     assert np.array_equal(chunked.positions, whole.positions)
     assert np.array_equal(chunked.fitness, whole.fitness)
     assert chunked.warnings == whole.warnings
+    if bound > 1e100:
+        assert whole.warnings - pop.warnings == cfg.ps  # every candidate is inf: one warning each, no more

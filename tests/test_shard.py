@@ -166,3 +166,78 @@ def test_virtual_partitions_equal_single_gpu_and_oracle(name, ps, dim, world):
     if not name.startswith("cec"):
         want = oracle.run(ps=ps, dim=dim, max_iterations=15, seed=11, name=name, lower=-100.0, upper=100.0)
         assert np.array_equal(pos, want["positions"]) and np.array_equal(trace, want["trace"])
+
+
+# ---------------------------------------------------------------------------- independent runs
+
+
+def oracle_batch(cfg, objs, seeds, want_trace=False):
+    """Test-only stand-in for run_batch: the oracle run per (objective, seed), packed like BatchResult."""
+    from paper_2510_14982_b200.engine import BatchResult
+
+    outs = [oracle.run(ps=cfg.ps, dim=cfg.dim, max_iterations=cfg.max_iterations, seed=int(s), name=o.name,
+                       lower=cfg.bounds.lower, upper=cfg.bounds.upper) for o, s in zip(objs, seeds)]
+    return BatchResult(best_fitness=np.array([o["best_fitness"] for o in outs]),
+                       best_position=np.stack([o["best_position"] for o in outs]),
+                       trace=np.stack([o["trace"] for o in outs]) if want_trace else None,
+                       warnings=np.array([o["warnings"] for o in outs], dtype=np.int64))
+
+
+RUN_MANY_NAMES = ["sphere", "rosenbrock", "griewank", "hgbat", "bent_cigar"]
+RUN_MANY_SEEDS = [0, 1, 2]
+
+
+def _run_many_worker(rank, world, port, cfg, q):
+    from paper_2510_14982_b200.engine import run_many
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        names = [n for n in RUN_MANY_NAMES for _ in RUN_MANY_SEEDS]
+        seeds = [s for _ in RUN_MANY_NAMES for s in RUN_MANY_SEEDS]
+        res = run_many(cfg, names, seeds, want_trace=True, batch_fn=oracle_batch)
+        q.put((rank, res.best_fitness, res.best_position, res.trace, res.warnings, res.objectives, res.seeds))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_run_many_round_robin_equals_serial(world):
+    """(objective, seed) runs round-robin over ranks, no collective while they run, one
+    all-gather at the end; every rank ends with all runs in submission order, equal to the serial loop of
+    the reference (engine.py:270-275) run by the oracle."""
+    cfg = ApoConfig(ps=20, dim=5, bounds=Bounds(-10.0, 10.0, 5), max_iterations=15, seed=0)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run_many_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    names = [n for n in RUN_MANY_NAMES for _ in RUN_MANY_SEEDS]
+    seeds = [s for _ in RUN_MANY_NAMES for s in RUN_MANY_SEEDS]
+    for rank, best, bpos, trace, warn, objs, sds in got:
+        assert list(objs) == names and list(sds) == seeds
+        for k, (n, s) in enumerate(zip(names, seeds)):
+            want = oracle.run(ps=20, dim=5, max_iterations=15, seed=s, name=n, lower=-10.0, upper=10.0)
+            assert best[k] == want["best_fitness"] and np.array_equal(bpos[k], want["best_position"]), (rank, k)
+            assert np.array_equal(trace[k], want["trace"]) and warn[k] == want["warnings"]
+
+
+@pytest.mark.gpu
+def test_run_many_single_process_equals_oracle():
+    """run_many at world size 1 is run_batch on the device: every run equals the oracle's serial run."""
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200.engine import run_many
+
+    cfg = pz.ApoConfig(ps=20, dim=5, bounds=pz.Bounds(-10.0, 10.0, 5), max_iterations=15, seed=0)
+    names = [n for n in RUN_MANY_NAMES for _ in RUN_MANY_SEEDS]
+    seeds = [s for _ in RUN_MANY_NAMES for s in RUN_MANY_SEEDS]
+    res = run_many(cfg, names, seeds, want_trace=True)
+    want = oracle_batch(cfg, [pz.get_objective(n) for n in names], seeds, want_trace=True)
+    assert np.array_equal(res.best_fitness, want.best_fitness)
+    assert np.array_equal(res.best_position, want.best_position)
+    assert np.array_equal(res.trace, want.trace) and np.array_equal(res.warnings, want.warnings)
