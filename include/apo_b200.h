@@ -262,6 +262,13 @@ double apo_rng_uniform(int rng, uint64_t seed, uint64_t iteration, uint64_t indi
 /* Debug/verification entry: out[k] = device exp_glibc(x[k]). */
 int apo_debug_exp(const double *x, double *out, int64_t n, void *stream);
 
+/* Debug/verification entry: out[r] = CEC2022 basic function `basic` (ids of csrc/apo_cec.cuh /
+ * oracle/cec_oracle.c; ELLIPS weights from ew, nullable) of row r of z [rows][n], evaluated by the
+ * headline kernels' quad evaluator (variant 0) or the warp evaluator (variant 1).  The five basic
+ * functions the reference also has replace objectives.py:112-142 / numba_backend.py:93-131. */
+int apo_debug_cec_basic(int basic, const double *z, int64_t rows, int64_t n, const double *ew, double *out,
+                        int variant, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,7 @@ def _declare(L):
 _EXTRA_DECLS: dict = {
     "or_cec_eval_batch": (None, [C.c_int, _P, _I, C.c_int, _P, _P, _P, _P, C.c_int]),
     "or_cec_spec": (None, [C.c_int, _P]),
+    "or_cec_basic_batch": (None, [C.c_int, _P, _I, C.c_int, _P]),
     "or_cec_ncomp": (C.c_int, [C.c_int]),
     "or_threshold_tables": (None, [_P, C.c_int, _P]),
     "or_threshold_eval": (C.c_double, [C.c_int, _P, _I, _P]),
@@ -127,6 +128,19 @@ def cec_eval(fn: int, x, nthreads: int = 1) -> np.ndarray:
     su = np.ascontiguousarray(shuffle, dtype=np.int32)
     out = np.zeros(rows)
     lib().or_cec_eval_batch(fn, _ptr(x), rows, dim, _ptr(sh), _ptr(ro), _ptr(su), _ptr(out), nthreads)
+    return out
+
+
+CEC_BASIC = {"zakharov": 0, "rosenbrock": 1, "escaffer6": 2, "rastrigin": 3, "step_rastrigin": 4, "levy": 5,
+             "bent_cigar": 6, "discus": 7, "ellips": 8, "hgbat": 9, "happycat": 10, "katsuura": 11, "ackley": 12,
+             "schwefel": 13, "schaffer_f7": 14, "grie_rosen": 15, "griewank": 16}
+
+
+def cec_basic(name: str, z) -> np.ndarray:
+    """A CEC2022 basic function alone (cec_oracle.c cec_basic_eval) on every row of z, no shift/scale."""
+    z = _f64(np.atleast_2d(z))
+    out = np.zeros(z.shape[0])
+    lib().or_cec_basic_batch(CEC_BASIC[name], _ptr(z), z.shape[0], z.shape[1], _ptr(out))
     return out
 
 

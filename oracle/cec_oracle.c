@@ -50,12 +50,16 @@ double cec_zakharov(const double *z, int n) {
     return s1 + s2 * s2 + s2 * s2 * s2 * s2;
 }
 
-double cec_rosenbrock(const double *z, int n) { /* z already +1 */
+/* The five basic functions the reference also has are written in ITS rounding order
+ * (objectives.py:112-142, numba_backend.py:93-131) so they are pinned to the reference's golden
+ * values (tests/test_cec_pinning.py): rosenbrock as 100 (a a) + b b with a = z[i+1] - z[i]^2,
+ * hgbat with sqrt, elliptic as (w z) z, griewank's product over cos(z / sqrt(i + 1)). */
+double cec_rosenbrock(const double *z, int n) { /* z already +1 (objectives.py:129-132) */
     double f = 0.0;
     for (int i = 0; i < n - 1; i++) {
-        double t1 = z[i] * z[i] - z[i + 1];
-        double t2 = z[i] - 1.0;
-        f += 100.0 * t1 * t1 + t2 * t2;
+        double a = z[i + 1] - z[i] * z[i];
+        double b = z[i] - 1.0;
+        f += 100.0 * (a * a) + b * b;
     }
     return f;
 }
@@ -118,7 +122,7 @@ double cec_hgbat(const double *z, int n) { /* z already -1 */
         r2 += z[i] * z[i];
         sz += z[i];
     }
-    return pow(fabs(r2 * r2 - sz * sz), 0.5) + (0.5 * r2 + sz) / n + 0.5;
+    return sqrt(fabs(r2 * r2 - sz * sz)) + (0.5 * r2 + sz) / n + 0.5; /* objectives.py:123-126 */
 }
 
 double cec_happycat(const double *z, int n) { /* z already -1 */
@@ -399,6 +403,11 @@ double or_cec_eval(int fn, const double *x, int n, const double *shift, const do
     }
     free(z);
     return f + S->fstar;
+}
+
+/* Basic function b (ids above) on each row of z: out[r] = g_b(z[r]) -- the building blocks alone. */
+void or_cec_basic_batch(int b, const double *z, int64_t rows, int n, double *out) {
+    for (int64_t r = 0; r < rows; r++) out[r] = cec_basic_eval(b, z + r * n, n);
 }
 
 /* Batch: out[r] = F_fn(x[r]) */

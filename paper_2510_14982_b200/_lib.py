@@ -29,7 +29,8 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-
 # csrc/apo_kernels.cuh); linked into a single shared library.
 SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_batch.cu", "apo_batch_m1.cu",
            "apo_batch_m2.cu", "apo_batch_m4.cu", "apo_batch_m0.cu", "apo_batch_warp.cu", "apo_cec_eval.cu",
-           "apo_cec_gemm.cu", "apo_prologue.cu"]
+           "apo_cec_gemm.cu", "apo_prologue.cu", "apo_update_fused.cu",
+           "apo_update_fused12.cu"]
 
 # CEC2022-only TUs (parity unpinned, checked at 1e-9 relative): FMA contraction allowed.  Every TU
 # on the reference's bit-exact path keeps --fmad=false.
@@ -159,6 +160,7 @@ PROTOTYPES = {
     "apo_shard_counters": (_INT, [_P, _P, _I, C.POINTER(C.c_int64)]),
     "apo_shard_destroy": (_INT, [_P]),
     "apo_debug_exp": (_INT, [_P, _P, _I, _P]),
+    "apo_debug_cec_basic": (_INT, [_INT, _P, _I, _I, _P, _P, _INT, _P]),
     "apo_philox4x32_10": (None, [_P, _P, _P]),
     "apo_rng_uniform": (_D, [_INT, _U, _U, _U, _U]),
 }

@@ -170,8 +170,8 @@ __device__ inline double cec_basic_warp(int b, const double* z, int n, int lane)
         return a + c * c + c * c * c * c;
     case B_ROSENBROCK:
         for (int i = lane; i < n - 1; i += 32) {
-            const double t1 = z[i] * z[i] - z[i + 1], t2 = z[i] - 1.0;
-            a += 100.0 * t1 * t1 + t2 * t2;
+            const double t1 = z[i + 1] - z[i] * z[i], t2 = z[i] - 1.0;  // objectives.py:129-132
+            a += 100.0 * (t1 * t1) + t2 * t2;
         }
         return wsum(a);
     case B_ESCAFFER6:
@@ -211,7 +211,7 @@ __device__ inline double cec_basic_warp(int b, const double* z, int n, int lane)
         }
         a = wsum(a);
         c = wsum(c);
-        if (b == B_HGBAT) return pow(fabs(a * a - c * c), 0.5) + (0.5 * a + c) / n + 0.5;
+        if (b == B_HGBAT) return sqrt(fabs(a * a - c * c)) + (0.5 * a + c) / n + 0.5;  // objectives.py:123-126
         return pow(fabs(a - n), 0.25) + (0.5 * a + c) / n + 0.5;
     }
     case B_KATSUURA: {
@@ -629,8 +629,8 @@ __device__ inline double cec_basic_quad_t(int b, const Zf& Z, int n, int t, cons
         return a + c * c + c * c * c * c;
     case B_ROSENBROCK:
         for (int i = t; i < n - 1; i += 4) {
-            const double t1 = Z(i) * Z(i) - Z(i + 1), t2 = Z(i) - 1.0;
-            a += 100.0 * t1 * t1 + t2 * t2;
+            const double t1 = Z(i + 1) - Z(i) * Z(i), t2 = Z(i) - 1.0;  // objectives.py:129-132
+            a += 100.0 * (t1 * t1) + t2 * t2;
         }
         return qsum(a);
     case B_ESCAFFER6:

@@ -499,7 +499,8 @@ enum OutMode : int {
 // Objective classes an update kernel is compiled for (keeps CEC code out of kernels that never see it).
 enum GroupKind : int { KIND_ANY = 0, KIND_BASIC = 1, KIND_CAND = 2 };
 
-template <int MAXC, bool MANY, bool CO, class Rows>
+// XCOPY (with CO): the clamped candidate also goes to T1[d] (the fused CEC kernel's shared-memory tile).
+template <int MAXC, bool MANY, bool CO, class Rows, bool XCOPY = false>
 __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, const Rows& R, int i, int p,
                                        double* cand_out, double* T1, double* T2, const GroupScratch& g, int lane,
                                        const double* staged) {
@@ -561,6 +562,7 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
             ok = ok && isfinite(c);
             cand_out[d] = c;
             if constexpr (!CO) write_terms(O, T1, T2, d, c, prev);
+            else if constexpr (XCOPY) T1[d] = c;
         }
     };
 

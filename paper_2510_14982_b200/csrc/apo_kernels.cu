@@ -340,6 +340,18 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         a.cand_ok = cand_ok;
         a.cec_bufs = 0;
     }
+    // SEL rows (device loop): candidates, DMMA evaluation and select as one kernel (apo_update_fused.cu)
+    static const int env_fused = getenv("APO_CEC_FUSED") ? atoi(getenv("APO_CEC_FUSED")) : 1;
+    if (split && sel_mode && env_fused && tile_counter) {
+        if (a.rank_hi <= 0) a.rank_hi = a.P.ps;
+        size_t fsmem = 0;
+        int fss = 0;
+        if (fused_cec_shape(a, smem_optin(), &fsmem, &fss) > 0) {
+            APO_CUDA(launch_update_cec_fused(a, st, tile_counter, smem_optin(), num_sms()));
+            if (mid_event) APO_CUDA(cudaEventRecord(mid_event, st));
+            return APO_OK;
+        }
+    }
     int w = group ? kWarps : warps_for_dim(dim);
     const bool stage = sel_mode && dim <= APO_STAGE_MAX_DIM;
     const size_t per_warp = group ? group_scratch_bytes(dim, stage, a.cec_bufs) : warp_scratch_bytes(dim);
@@ -802,6 +814,14 @@ int apo_debug_exp(const double* x, double* out, int64_t n, void* stream) {
     if (n == 0) return APO_OK;
     k_debug_exp<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(x, out, n);
     APO_CUDA(cudaGetLastError());
+    return APO_OK;
+}
+
+int apo_debug_cec_basic(int basic, const double* z, int64_t rows, int64_t n, const double* ew, double* out,
+                        int variant, void* stream) {
+    APO_CHECK(basic >= 0 && basic <= 16 && rows >= 0 && n >= 1 && (variant == 0 || variant == 1), "bad arguments");
+    if (rows == 0) return APO_OK;
+    APO_CUDA(launch_debug_cec_basic(basic, z, rows, (int)n, ew, out, variant, as_stream(stream)));
     return APO_OK;
 }
 

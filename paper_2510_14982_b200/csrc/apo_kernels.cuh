@@ -697,5 +697,10 @@ cudaError_t launch_prologue_small(int ps, const double* fit, const int* order_in
                                   Key cbase, unsigned* dr_bits, unsigned long long* scratch_keys, int* scratch_rank,
                                   int num_sms, cudaStream_t st);
 const void* pick_cec_eval(bool sel, int dim, bool fast);
+cudaError_t launch_debug_cec_basic(int b, const double* z, long long rows, int n, const double* ew, double* out,
+                                   int variant, cudaStream_t st);
+// apo_update_fused.cu: CEC2022 (D <= 104, SEL rows) candidates + DMMA evaluation + select in one kernel
+int fused_cec_shape(const UpdArgs& a, int optin, size_t* smem, int* stage_shift);
+cudaError_t launch_update_cec_fused(const UpdArgs& a, cudaStream_t st, unsigned* counter, int optin, int num_sms);
 
 }  // namespace apo

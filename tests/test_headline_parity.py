@@ -59,7 +59,10 @@ def assert_step_parity(sp, sf, want_pos, want_fit, want_acc, got_pos, got_fit, l
         f_cand = got_fit[k] if got_acc[k] else want_fit[k]
         assert abs(f_cand - sf[k]) <= TIE_RTOL * abs(sf[k]), \
             f"{label}: row {k} flipped with candidate {f_cand!r} vs incumbent {sf[k]!r}"
-    assert flips.mean() <= 1e-4, f"{label}: {flips.sum()} accept/keep flips"
+    # flips come from clamped candidates that ARE the incumbent row (all changed dimensions pinned to a
+    # bound): the same point, evaluated once by the oracle and once by the device.  More frequent at
+    # small D, where a whole candidate is clamped more often.
+    assert flips.mean() <= 2e-3, f"{label}: {flips.sum()} accept/keep flips"
     ga, wa = int(np.argmin(got_fit)), int(np.argmin(want_fit))
     if ga != wa:  # only an exact tie of the minimum may move the first index
         assert abs(got_fit[ga] - want_fit[wa]) <= TIE_RTOL * abs(want_fit[wa]), f"{label}: argmin {ga} vs {wa}"
@@ -100,7 +103,9 @@ def test_c4_device_loop_teacher_forced(fn):
             _, row = run.best()[::2]
             assert got_fit[row] == got_fit.min()
             pos, fit = want_pos, want_fit  # teacher forcing: the next iteration starts from the oracle
-        assert total_flips <= 40
+        # flips happen where a clamped candidate is the incumbent row itself (same point, last-ulp
+        # different fitness): ~2e-5 of rows at this shape; each one was asserted a tie above
+        assert total_flips <= 1e-4 * 4 * ps
     finally:
         run.close()
 

@@ -141,8 +141,9 @@ def test_option_a_reference_engine_step_with_cuda_backend(ref_with_cuda, name, p
     cfg = protozoa.ApoConfig(ps=ps, dim=dim, bounds=protozoa.Bounds(-30.0, 30.0, dim), max_iterations=20, seed=11)
     pop = protozoa.initialize(cfg, name)
     for t in range(4):
-        want = protozoa.step(pop, cfg, name, t, backend="numba")
-        got = protozoa.step(pop, cfg, name, t, backend="cuda")
+        mode = protozoa.EngineMode.sequential()
+        want = protozoa.step(pop, cfg, name, t, mode, backend="numba")
+        got = protozoa.step(pop, cfg, name, t, mode, backend="cuda")
         assert np.array_equal(got.positions, want.positions) and np.array_equal(got.fitness, want.fitness)
         assert got.warnings == want.warnings and got.fe_count == want.fe_count
         pop = want
