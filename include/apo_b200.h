@@ -122,6 +122,15 @@ int apo_run_updates_range(const double *positions, const double *fitness, const 
                           double eps, double p_ah, double f_mult, double decay, const apo_objective *objective_host,
                           const double *p_dr, unsigned long long *warn_count, int64_t rank_lo, int64_t rank_hi,
                           void *stream);
+/* apo_run_updates_range without the snapshot gather (core.py:504-513's row copy): positions/fitness
+ * stay in the caller's row order and order[r] (int32, the stable sort's rank -> row map, apo_sort_order)
+ * names the row holding rank r; outputs are by rank, as apo_run_updates writes them.  dim <= 256. */
+int apo_run_updates_ordered(const double *positions, const double *fitness, const int32_t *order,
+                            const uint8_t *in_dr, double *out_pos, double *out_fit, uint8_t *out_acc,
+                            uint8_t *out_warn, int64_t ps, int64_t dim, uint64_t seed, uint64_t key_iteration,
+                            int64_t npairs, double lower, double upper, double eps, double p_ah, double f_mult,
+                            double decay, const apo_objective *objective_host, const double *p_dr,
+                            unsigned long long *warn_count, int64_t rank_lo, int64_t rank_hi, void *stream);
 
 /* Batch fitness: out[r] = f(x[r*ld .. r*ld+dim)) (objectives.evaluate_unchecked,
  * objectives.py:222-228). */
@@ -192,6 +201,10 @@ int apo_run_profile_read(apo_run *run, double *update_ms_host, int64_t *launches
 /* Same, split at the boundary between the candidate kernel and the CEC2022
  * evaluation kernel (k_cec_eval; evaluate_ms is 0 for fused objectives). */
 int apo_run_profile_split(apo_run *run, double *candidates_ms_host, double *evaluate_ms_host, int64_t *launches_host);
+/* Which kernels one iteration's update runs: 0 one fused kernel (basic objectives), 1 CEC2022 split
+ * (candidates, then the DMMA evaluation kernel), 2 CEC2022 fused (one kernel: candidates + DMMA
+ * evaluation + select), 3 CEC2022 at D > 104 (candidates, DMMA GEMM, finish). */
+int apo_run_update_path(apo_run *run, int *path_host);
 
 /*
  * One population sharded by rank across processes (engine.run with the

@@ -124,6 +124,8 @@ PROTOTYPES = {
                                    C.POINTER(apo_objective), _P, _P, _P]),
     "apo_run_updates_range": (_INT, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _U, _U, _I, _D, _D, _D, _D, _D, _D,
                                      C.POINTER(apo_objective), _P, _P, _I, _I, _P]),
+    "apo_run_updates_ordered": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _U, _U, _I, _D, _D, _D, _D, _D, _D,
+                                       C.POINTER(apo_objective), _P, _P, _I, _I, _P]),
     "apo_evaluate": (_INT, [_P, _I, _I, _I, C.POINTER(apo_objective), _P, _P]),
     "apo_initialize": (_INT, [_U, _I, _I, _I, _D, _D, C.POINTER(apo_objective), _P, _P, _P]),
     "apo_sort_order": (_INT, [_P, _I, _P, _P]),
@@ -143,6 +145,7 @@ PROTOTYPES = {
     "apo_run_profile": (_INT, [_P, _INT]),
     "apo_run_profile_read": (_INT, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "apo_run_profile_split": (_INT, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "apo_run_update_path": (_INT, [_P, C.POINTER(_INT)]),
     "apo_run_batch": (_INT, [_I, _P, C.POINTER(apo_objective), _I, _I, _I, _I, _I, _D, _D, _D, _D, _P, _P, _P, _P,
                              _P, _P, _P, _P, _INT, _P]),
     "apo_run_batch_shaped": (_INT, [_I, _P, C.POINTER(apo_objective), _I, _I, _I, _I, _I, _D, _D, _D, _D, _P, _P,

@@ -611,6 +611,20 @@ __device__ __forceinline__ void cec_rotate_quad(const double* __restrict__ rot_p
     __syncwarp();
 }
 
+// Rotation by component k's matrix: the shared-memory copy when the CTA staged this component, else
+// rot_pad through L1.  Two call sites on purpose: a pointer selected between the two would be generic
+// and turn every B-fragment load into a generic LD instead of LDS.
+template <int NT>
+__device__ __forceinline__ void cec_rotate_comp(const CecData& C, const double* bsm, bool staged, int k, double* Y,
+                                                int ys, int n, double off, int lane) {
+    if (staged) {
+        cec_rotate_quad<NT>(bsm, Y, ys, n, off, lane, 8 * NT + 4);
+    } else {
+        const int n4 = (n + 3) & ~3;
+        cec_rotate_quad<NT>(C.rot_pad + (size_t)k * n4 * (8 * NT), Y, ys, n, off, lane, 8 * NT);
+    }
+}
+
 // Basic function b over z[0..n) by the 4 lanes of a quad; every lane of the
 // quad returns the value.  ew: host-computed ELLIPS weights (nullable).
 // Z(i): element i of the basic function's input (a stored row, or an affine map of the candidate
@@ -743,8 +757,7 @@ __device__ inline double cec_eval_quad(const CecData& C, double* X, const double
     // bsm: shared-memory copy (row stride 8 NT + 4) of rotation `bsm_comp`, the others via L1.
     // src: this quad's candidate row in global memory (nullptr for a dead row): compositions
     // re-read it for every component instead of keeping a second copy in shared memory.
-    const double* B0 = (bsm && bsm_comp == 0) ? bsm : C.rot_pad;
-    const int bs0 = (bsm && bsm_comp == 0) ? 8 * NT + 4 : 8 * NT;
+    const bool staged0 = bsm && bsm_comp == 0;
     const CecSpec& S = kCecSpec[C.fn - 1];
     const int q = lane >> 2, t = lane & 3;
     const int n4 = (n + 3) & ~3;
@@ -760,14 +773,14 @@ __device__ inline double cec_eval_quad(const CecData& C, double* X, const double
             x[i] = (xi - oi) * sc;
         }
         __syncwarp();
-        cec_rotate_quad<NT>(B0, X, xs, n, cec_offset(b), lane, bs0);
+        cec_rotate_comp<NT>(C, bsm, staged0, 0, X, xs, n, cec_offset(b), lane);
         f = cec_basic_quad(b, x, n, t, ew);
     } else if (S.kind == 1) {
         // rot_pad's output columns are pre-permuted by the shuffle (objectives.py), so the rotation
         // leaves z[shuffle[j]-1] in column j: the segments are contiguous, no gather
         for (int i = t; i < n; i += 4) x[i] = x[i] - C.shift[i];
         __syncwarp();
-        cec_rotate_quad<NT>(B0, X, xs, n, 0.0, lane, bs0);
+        cec_rotate_comp<NT>(C, bsm, staged0, 0, X, xs, n, 0.0, lane);
         int sizes[6];
         int tot = 0;
         for (int k = 0; k < S.ncomp - 1; k++) {
@@ -826,9 +839,7 @@ __device__ inline double cec_eval_quad(const CecData& C, double* X, const double
                         }
                         d2 = qsum(d2);
                         __syncwarp();
-                        const bool sm = bsm && bsm_comp == k;
-                        cec_rotate_quad<NT>(sm ? bsm : C.rot_pad + (size_t)k * n4 * (8 * NT), X, xs, n, off, lane,
-                                            sm ? 8 * NT + 4 : 8 * NT);
+                        cec_rotate_comp<NT>(C, bsm, bsm && bsm_comp == k, k, X, xs, n, off, lane);
                         fit[k] = S.lam[k] * cec_basic_quad(b, x, n, t, ew) + S.bias[k];
                         x_intact = false;
                     }
@@ -858,9 +869,7 @@ __device__ inline double cec_eval_quad(const CecData& C, double* X, const double
                 d2 = qsum(d2);
                 __syncwarp();
                 if (rot) {
-                    const bool sm = bsm && bsm_comp == k;
-                    cec_rotate_quad<NT>(sm ? bsm : C.rot_pad + (size_t)k * n4 * (8 * NT), X, xs, n, off, lane,
-                                        sm ? 8 * NT + 4 : 8 * NT);
+                    cec_rotate_comp<NT>(C, bsm, bsm && bsm_comp == k, k, X, xs, n, off, lane);
                 }
                 fit[k] = S.lam[k] * cec_basic_quad(b, x, n, t, ew) + S.bias[k];
                 __syncwarp();

@@ -325,6 +325,24 @@ int smem_optin() {
 int launch_cec_eval(bool sel_mode, const UpdArgs& a, cudaStream_t st, uint8_t* cand_ok, unsigned* tile_counter,
                     int init);
 
+// Which kernels an update launch runs (apo_run_update_path): 0 one fused kernel (basic objectives,
+// or CEC2022 without DMMA tables), 1 CEC2022 split (k_update_group candidates + k_cec_eval), 2 fused
+// CEC2022 (k_update_cec), 3 CEC2022 GEMM (candidates + k_dgemm_nn + k_cec_finish).
+int update_path(bool sel_mode, const UpdArgs& a, bool have_cand_ok, bool have_counter) {
+    const int dim = a.P.dim;
+    const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
+    const bool cec = have_cand_ok && a.O.code > APO_OBJ_CEC2022_BASE;
+    if (cec && dim <= kGroupMaxDim && dim <= kCecEvalMaxDim && a.O.cec.rot_pad != nullptr) {
+        const int env_fused = getenv("APO_CEC_FUSED") ? atoi(getenv("APO_CEC_FUSED")) : 0;  // off: slower
+        size_t fsmem = 0;
+        int fss = 0;
+        if (sel_mode && env_fused && have_counter && fused_cec_shape(a, smem_optin(), &fsmem, &fss) > 0) return 2;
+        return 1;
+    }
+    if (cec && dim > kCecEvalMaxDim && a.O.cec.rot_gemm != nullptr && (fn_id <= 8 || fn_id == 10)) return 3;
+    return 0;
+}
+
 int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* cand_ok = nullptr,
                   cudaEvent_t mid_event = nullptr, unsigned* tile_counter = nullptr) {
     UpdArgs a = A0;
@@ -341,16 +359,11 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         a.cec_bufs = 0;
     }
     // SEL rows (device loop): candidates, DMMA evaluation and select as one kernel (apo_update_fused.cu)
-    static const int env_fused = getenv("APO_CEC_FUSED") ? atoi(getenv("APO_CEC_FUSED")) : 1;
-    if (split && sel_mode && env_fused && tile_counter) {
+    if (split && update_path(sel_mode, a, true, tile_counter != nullptr) == 2) {
         if (a.rank_hi <= 0) a.rank_hi = a.P.ps;
-        size_t fsmem = 0;
-        int fss = 0;
-        if (fused_cec_shape(a, smem_optin(), &fsmem, &fss) > 0) {
-            APO_CUDA(launch_update_cec_fused(a, st, tile_counter, smem_optin(), num_sms()));
-            if (mid_event) APO_CUDA(cudaEventRecord(mid_event, st));
-            return APO_OK;
-        }
+        APO_CUDA(launch_update_cec_fused(a, st, tile_counter, smem_optin(), num_sms()));
+        if (mid_event) APO_CUDA(cudaEventRecord(mid_event, st));
+        return APO_OK;
     }
     int w = group ? kWarps : warps_for_dim(dim);
     const bool stage = sel_mode && dim <= APO_STAGE_MAX_DIM;
@@ -611,12 +624,44 @@ int apo_run_updates_obj(const double* positions, const double* fitness, const ui
                                  warn_count, 0, ps, stream);
 }
 
+namespace {
+int updates_range(const double* positions, const double* fitness, const int32_t* order, const uint8_t* in_dr,
+                  double* out_pos, double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim,
+                  uint64_t seed, uint64_t key_iteration, int64_t npairs, double lower, double upper, double eps,
+                  double p_ah, double f_mult, double decay, const apo_objective* objective_host, const double* p_dr,
+                  unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi, void* stream);
+}
+
 int apo_run_updates_range(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
                           double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim,
                           uint64_t seed, uint64_t key_iteration, int64_t npairs, double lower, double upper,
                           double eps, double p_ah, double f_mult, double decay, const apo_objective* objective_host,
                           const double* p_dr, unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi,
                           void* stream) {
+    return updates_range(positions, fitness, nullptr, in_dr, out_pos, out_fit, out_acc, out_warn, ps, dim, seed,
+                         key_iteration, npairs, lower, upper, eps, p_ah, f_mult, decay, objective_host, p_dr,
+                         warn_count, rank_lo, rank_hi, stream);
+}
+
+int apo_run_updates_ordered(const double* positions, const double* fitness, const int32_t* order,
+                            const uint8_t* in_dr, double* out_pos, double* out_fit, uint8_t* out_acc,
+                            uint8_t* out_warn, int64_t ps, int64_t dim, uint64_t seed, uint64_t key_iteration,
+                            int64_t npairs, double lower, double upper, double eps, double p_ah, double f_mult,
+                            double decay, const apo_objective* objective_host, const double* p_dr,
+                            unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi, void* stream) {
+    APO_CHECK(order != nullptr, "order is NULL");
+    APO_CHECK(dim <= kGroupMaxDim, "apo_run_updates_ordered: dim > 256 (gather the snapshot, use _range)");
+    return updates_range(positions, fitness, order, in_dr, out_pos, out_fit, out_acc, out_warn, ps, dim, seed,
+                         key_iteration, npairs, lower, upper, eps, p_ah, f_mult, decay, objective_host, p_dr,
+                         warn_count, rank_lo, rank_hi, stream);
+}
+
+namespace {
+int updates_range(const double* positions, const double* fitness, const int32_t* order, const uint8_t* in_dr,
+                  double* out_pos, double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim,
+                  uint64_t seed, uint64_t key_iteration, int64_t npairs, double lower, double upper, double eps,
+                  double p_ah, double f_mult, double decay, const apo_objective* objective_host, const double* p_dr,
+                  unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi, void* stream) {
     APO_CHECK(ps >= 1 && ps < (1LL << 31), "ps out of range");
     APO_CHECK(0 <= rank_lo && rank_lo < rank_hi && rank_hi <= ps, "rank range must satisfy 0 <= lo < hi <= ps");
     APO_CHECK(dim >= 1 && dim <= 8192, "dim out of range (1..8192)");
@@ -653,6 +698,7 @@ int apo_run_updates_range(const double* positions, const double* fitness, const 
     A.out_acc = out_acc;
     A.out_warn = out_warn;
     A.warn_count = warn_count;
+    A.order = order;  // rows of positions/fitness read at order[rank]; outputs by rank
     A.cec_bufs = cec_bufs_for(A.O.code);
     uint8_t* cand_ok = nullptr;
     const bool cec = A.O.code > APO_OBJ_CEC2022_BASE;
@@ -663,6 +709,7 @@ int apo_run_updates_range(const double* positions, const double* fitness, const 
     if (cec) cudaFreeAsync(cand_ok, as_stream(stream));
     return rc;
 }
+}  // namespace
 
 int apo_run_updates(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
                     double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim, uint64_t seed,
@@ -1120,6 +1167,17 @@ int apo_run_profile(apo_run* r, int enable) {
     APO_CUDA(cudaStreamSynchronize(r->stream));
     clear_profile(r);
     r->profile = enable != 0;
+    return APO_OK;
+}
+
+int apo_run_update_path(apo_run* r, int* path_host) {
+    APO_CHECK(r && path_host, "NULL argument");
+    UpdArgs A{};
+    A.P.dim = (int)r->dim;
+    A.P.ps = (int)r->ps;
+    A.P.npairs = (int)r->npairs;
+    A.O = r->obj;
+    *path_host = update_path(true, A, true, true);
     return APO_OK;
 }
 

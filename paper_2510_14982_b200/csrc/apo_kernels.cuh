@@ -515,7 +515,6 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     const int dim = A.dim, cs = cec_stride(dim), n4 = (dim + 3) & ~3;
     const bool pf = FAST && A.prefetch;
     double* base = reinterpret_cast<double*>(smem + (size_t)warp * cec_eval_warp_bytes(dim, A.bufs, pf));
-    double* Xb[2] = {base, base + (size_t)kCecRows * cs};
     double* bsm = nullptr;
     CecData C = A.O.cec;
     if constexpr (FAST) {
@@ -540,7 +539,7 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     auto live_in = [&](int tile) { return tile < ntiles && row_of(tile) < A.row0 + A.n_rows; };
     // row q of `tile` -> X tile `buf` (cp.async); pads and dead rows are zero
     auto issue = [&](int tile, int buf, uint8_t selq) {
-        double* xrow = Xb[buf] + (size_t)q * cs;
+        double* xrow = base + (size_t)buf * kCecRows * cs + (size_t)q * cs;
         const bool live = live_in(tile);
         const double* src = nullptr;
         if (live) {
@@ -611,7 +610,8 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
         __syncwarp();
         const double* qsrc = nullptr;  // this quad's candidate row (compositions re-read it per component)
         if (live) qsrc = SEL ? (cur || A.init ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
-        const double nf = cec_eval_quad<NT>(C, Xb[buf], qsrc, cs, dim, lane, ew, bsm, A.bsm_comp);
+        const double nf = cec_eval_quad<NT>(C, base + (size_t)buf * kCecRows * cs, qsrc, cs, dim, lane, ew, bsm,
+                                            A.bsm_comp);
         bool acc = false;
         if (A.init) {  // iteration 0 (engine.py:116-139): the fitness of every initial row
             if (live && t == 0) {

@@ -28,7 +28,7 @@ int fused_cec_shape(const UpdArgs& a, int optin, size_t* smem, int* stage_shift)
             (fused_rot_bytes(dim, nt) + (ss ? 8 * (size_t)((ncomp * dim + 1) & ~1) : 0) + 15) & ~(size_t)15;
         if (head >= (size_t)avail) continue;
         int w = (int)(((size_t)avail - head) / fused_warp_bytes(dim));
-        static const int env_w = getenv("APO_FUSED_WARPS") ? atoi(getenv("APO_FUSED_WARPS")) : 16;
+        const int env_w = getenv("APO_FUSED_WARPS") ? atoi(getenv("APO_FUSED_WARPS")) : 16;
         if (w > env_w) w = env_w;
         w = w >= 16 ? 16 : w >= 12 ? 12 : 0;  // the instantiated CTA shapes
         if (w > 0) {

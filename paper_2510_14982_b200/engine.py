@@ -171,23 +171,41 @@ def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: Engin
     lib = _lib.require_cuda()
     dev = _dev()
     stream = _lib.stream_handle()
-    pos = _to_device(pop.positions, dev)
+    lean = cfg.ps >= STEP_CHUNK_MIN_PS and bk.NAME == "cuda" and cfg.dim <= 256
+    main = torch.cuda.current_stream()
+    # fitness first (8 bytes per row): the stable sort and the coordinator draws run while the rows
+    # stream in on a second stream
     fit = _to_device(pop.fitness, dev)
+    if lean:
+        copy = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(copy):
+            pos = _to_device(pop.positions, dev)
+        pos.record_stream(main)
+    else:
+        pos = _to_device(pop.positions, dev)
     order = torch.empty(cfg.ps, dtype=torch.int32, device=dev)
     _lib.check(lib.apo_sort_order(_lib.ptr(fit), cfg.ps, _lib.ptr(order), stream), "apo_sort_order")
-    order = order.long()
-    snap_pos = pos.index_select(0, order).contiguous()
-    snap_fit = fit.index_select(0, order).contiguous()
     in_dr = torch.empty(cfg.ps, dtype=torch.uint8, device=dev)
     _lib.check(lib.apo_select_dr(cfg.seed, iteration + 1, cfg.ps, cfg.pf_max, _lib.ptr(in_dr), None, stream),
                "apo_select_dr")
-    if cfg.ps >= STEP_CHUNK_MIN_PS and bk.NAME == "cuda":
-        # large populations: copy finished rank chunks back while the next chunk updates
+    if lean:
+        # large populations: no snapshot gather (the update reads rows through order[]); finished rank
+        # chunks are copied back while the next chunk updates
         from .kernels import cuda_backend
 
-        hp, hf, warned = cuda_backend.run_updates_to_host(snap_pos, snap_fit, in_dr, cfg, obj, iteration,
-                                                          iteration + 1)
+        main.wait_stream(copy)
+        hp, hf, warned = cuda_backend.run_updates_to_host(pos, fit, in_dr, cfg, obj, iteration, iteration + 1,
+                                                          order=order)
+    elif cfg.ps >= STEP_CHUNK_MIN_PS and bk.NAME == "cuda":  # D > 256: the warp kernel reads rank-ordered rows
+        from .kernels import cuda_backend
+
+        idx = order.long()
+        hp, hf, warned = cuda_backend.run_updates_to_host(pos.index_select(0, idx), fit.index_select(0, idx), in_dr,
+                                                          cfg, obj, iteration, iteration + 1)
     else:
+        idx = order.long()
+        snap_pos = pos.index_select(0, idx).contiguous()
+        snap_fit = fit.index_select(0, idx).contiguous()
         new_pos, new_fit, _acc, warned = bk.run_updates(snap_pos, snap_fit, in_dr, cfg, obj, iteration,
                                                         iteration + 1, parallel=(mode.kind == PARALLEL),
                                                         workers=workers)
@@ -279,6 +297,12 @@ class DeviceRun:
         _lib.check(self.lib.apo_run_profile_split(self.handle, C.byref(a), C.byref(b), C.byref(n)),
                    "apo_run_profile_split")
         return a.value, b.value, n.value
+
+    def update_path(self) -> str:
+        """Kernels of one iteration's update: "fused" (basic objectives), "cec_split", "cec_fused", "cec_gemm"."""
+        p = C.c_int()
+        _lib.check(self.lib.apo_run_update_path(self.handle, C.byref(p)), "apo_run_update_path")
+        return ("fused", "cec_split", "cec_fused", "cec_gemm")[p.value]
 
     def close(self):
         if self.handle:

@@ -77,11 +77,12 @@ def run_updates(positions, fitness, in_dr, cfg: ApoConfig, objective: Objective,
 
 
 def run_updates_to_host(pos, fit, in_dr, cfg: ApoConfig, objective: Objective, iteration: int, key_iteration: int,
-                        chunks: int = 4):
+                        chunks: int = 4, order=None):
     """run_updates on device tensors with the result delivered to page-locked host memory: the update
     runs in rank chunks (apo_run_updates_range) and each finished chunk is copied back on a second
     stream while the next one computes.  Returns (positions, fitness) numpy views and the warning count;
-    bit-identical to run_updates."""
+    bit-identical to run_updates.  With `order` (int32 rank -> row, the stable sort's result) pos/fit
+    are NOT the rank-ordered snapshot but the caller's rows, read through order[] (no gather)."""
     import torch
 
     lib = _lib.require_cuda()
@@ -101,11 +102,18 @@ def run_updates_to_host(pos, fit, in_dr, cfg: ApoConfig, objective: Objective, i
     step = (step + 31) // 32 * 32
     for lo in range(0, ps, step):
         hi = min(ps, lo + step)
-        _lib.check(lib.apo_run_updates_range(
-            _lib.ptr(pos), _lib.ptr(fit), _lib.ptr(in_dr), _lib.ptr(out_pos), _lib.ptr(out_fit), None, None,
-            ps, dim, cfg.seed, key_iteration, cfg.neighbor_pairs, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,
-            p_ah, f_mult, decay, dobj.ref, _lib.ptr(pdr), _lib.ptr(warn), lo, hi, _lib.stream_handle()),
-            "apo_run_updates_range")
+        if order is not None:
+            _lib.check(lib.apo_run_updates_ordered(
+                _lib.ptr(pos), _lib.ptr(fit), _lib.ptr(order), _lib.ptr(in_dr), _lib.ptr(out_pos), _lib.ptr(out_fit),
+                None, None, ps, dim, cfg.seed, key_iteration, cfg.neighbor_pairs, cfg.bounds.lower,
+                cfg.bounds.upper, cfg.eps, p_ah, f_mult, decay, dobj.ref, _lib.ptr(pdr), _lib.ptr(warn), lo, hi,
+                _lib.stream_handle()), "apo_run_updates_ordered")
+        else:
+            _lib.check(lib.apo_run_updates_range(
+                _lib.ptr(pos), _lib.ptr(fit), _lib.ptr(in_dr), _lib.ptr(out_pos), _lib.ptr(out_fit), None, None,
+                ps, dim, cfg.seed, key_iteration, cfg.neighbor_pairs, cfg.bounds.lower, cfg.bounds.upper, cfg.eps,
+                p_ah, f_mult, decay, dobj.ref, _lib.ptr(pdr), _lib.ptr(warn), lo, hi, _lib.stream_handle()),
+                "apo_run_updates_range")
         copy.wait_stream(compute)
         with torch.cuda.stream(copy):
             hp[lo:hi].copy_(out_pos[lo:hi], non_blocking=True)

@@ -19,6 +19,9 @@ the kernels are ordered):
 3. all-gather of rows [lo, hi) of the next position/fitness buffers (NCCL
    over NVLink), so every process again holds the whole population -- now in
    rank order, which is exactly the reference's row order (engine.py:167-172).
+   Each process's ranks come in `blocks` pieces (ShardPlan), and the gather of
+   piece s is issued asynchronously as soon as it is updated, so NVLink
+   traffic overlaps the update of piece s+1.
 
 Traffic per iteration and GPU: (N-1)/N of the population (8 * ps * ld bytes)
 received; SURVEY.md §8e explains why that bounds strong scaling at D = 100.
@@ -41,23 +44,37 @@ GROUP = 32  # the update kernel owns ranks in groups of 32 (apo_group.cuh)
 
 @dataclass(frozen=True)
 class ShardPlan:
-    """Rank ranges of a population split over `world` processes, in whole groups of 32."""
+    """Rank ranges of a population split over `world` processes, in whole groups of 32.
+
+    With blocks = S > 1 the ranks are dealt out in S rounds: block s of process r is the range of
+    `chunk` ranks starting at (s * world + r) * chunk.  Block s of every process is then one contiguous
+    span of the buffer, so it can be all-gathered in place as soon as it is updated while block s+1
+    computes (which process updates a rank is free: every process holds the whole population)."""
 
     ps: int
     world: int
+    blocks: int = 1
 
     @property
     def chunk(self) -> int:
-        per = -(-self.ps // self.world)
+        per = -(-self.ps // (self.world * self.blocks))
         return -(-per // GROUP) * GROUP
 
     @property
     def ps_pad(self) -> int:
-        return self.chunk * self.world
+        return self.chunk * self.world * self.blocks
+
+    def block(self, rank: int, s: int) -> tuple:
+        lo = min((s * self.world + rank) * self.chunk, self.ps)
+        return lo, min(lo + self.chunk, self.ps)
+
+    def ranges(self, rank: int) -> list:
+        return [self.block(rank, s) for s in range(self.blocks)]
 
     def range(self, rank: int) -> tuple:
-        lo = min(rank * self.chunk, self.ps)
-        return lo, min(lo + self.chunk, self.ps)
+        if self.blocks != 1:
+            raise ValueError("range() is for single-block plans; use ranges()")
+        return self.block(rank, 0)
 
 
 def _dist(group):
@@ -154,17 +171,23 @@ class ShardedRun:
     process: the same kernels and layout without the exchange -- used to check partition independence)."""
 
     def __init__(self, cfg: ApoConfig, objective, group=None, virtual_world: Optional[int] = None, stream=None,
-                 engine=None):
+                 engine=None, blocks: Optional[int] = None):
         self.cfg = cfg
         self.obj = resolve_objective(objective)
         self.dist, self.world, self.rank = _dist(group)
         self.group = group
+        # blocks per process: the exchange of block s overlaps the update of block s+1 (4 by default when
+        # there is an exchange; never more than one group of 32 ranks per block and process)
+        world = virtual_world if virtual_world is not None else self.world
+        if blocks is None:
+            blocks = 4 if self.world > 1 else 1
+        blocks = max(1, min(int(blocks), -(-cfg.ps // (GROUP * world))))
         if virtual_world is not None:
             if self.world != 1:
                 raise ValueError("virtual_world is for single-process runs")
-            self.plan = ShardPlan(cfg.ps, virtual_world)
+            self.plan = ShardPlan(cfg.ps, virtual_world, blocks)
         else:
-            self.plan = ShardPlan(cfg.ps, self.world)
+            self.plan = ShardPlan(cfg.ps, self.world, blocks)
         self.virtual = virtual_world is not None
         # `engine` replaces the device shard only in tests of this orchestration (tests/test_shard.py)
         self.dev = engine(cfg, self.obj, self.plan) if engine is not None else _DeviceShard(cfg, self.obj, self.plan,
@@ -175,12 +198,17 @@ class ShardedRun:
         self.dev.initialize()
         self.iterations = 0
 
-    def _exchange(self):
+    def _exchange_block(self, s: int):
+        """Start the in-place all-gather of block s (rows + fitness) of the next buffers; NCCL runs it on
+        its own stream, so the update of block s+1 proceeds on the compute stream meanwhile."""
         pos, fit = self.dev.next_buffers()
-        c = self.plan.chunk
-        lo = self.rank * c
-        self.dist.all_gather_into_tensor(pos, pos[lo:lo + c], group=self.group)  # in place
-        self.dist.all_gather_into_tensor(fit, fit[lo:lo + c], group=self.group)
+        c, w = self.plan.chunk, self.world
+        base = s * w * c
+        mine = base + self.rank * c
+        return [self.dist.all_gather_into_tensor(pos[base:base + w * c], pos[mine:mine + c], group=self.group,
+                                                 async_op=True),
+                self.dist.all_gather_into_tensor(fit[base:base + w * c], fit[mine:mine + c], group=self.group,
+                                                 async_op=True)]
 
     def iterate(self, n: int):
         if self.iterations + n > self.cfg.max_iterations:
@@ -189,11 +217,16 @@ class ShardedRun:
             self.dev.begin()
             if self.virtual:
                 for r in range(self.plan.world):
-                    self.dev.update_range(*self.plan.range(r))
+                    for lo, hi in self.plan.ranges(r):
+                        self.dev.update_range(lo, hi)
             else:
-                self.dev.update_range(*self.plan.range(self.rank))
-                if self.world > 1:
-                    self._exchange()
+                works = []
+                for s, (lo, hi) in enumerate(self.plan.ranges(self.rank)):
+                    self.dev.update_range(lo, hi)
+                    if self.world > 1:
+                        works += self._exchange_block(s)
+                for wk in works:  # the compute stream waits for every block before the next sort
+                    wk.wait()
             self.dev.end()
             self.iterations += 1
 

@@ -364,3 +364,49 @@ def test_step_chunked_d2h_matches_single_launch(pz, name, dim, bound, monkeypatc
     assert chunked.warnings == whole.warnings
     if bound > 1e100:
         assert whole.warnings - pop.warnings == cfg.ps  # every candidate is inf: one warning each, no more
+
+
+@pytest.mark.parametrize("name,dim", [("rosenbrock", 30), ("cec2022_f6", 100), ("cec2022_f10", 40),
+                                      ("cec2022_f1", 150), ("hgbat", 200)])
+def test_ordered_update_equals_gathered_snapshot(pz, name, dim):
+    """apo_run_updates_ordered (rows read through the sort's rank -> row map, no gather) equals
+    apo_run_updates_range on the gathered snapshot, bit for bit, on every update path (group, CEC
+    split, CEC GEMM) and per rank chunk."""
+    import torch
+
+    from paper_2510_14982_b200 import _lib
+    from paper_2510_14982_b200.core import iteration_scalars
+    from paper_2510_14982_b200.kernels.cuda_backend import p_dr_device
+    from paper_2510_14982_b200.objectives import device_objective
+
+    ps = 5000
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=20, seed=13)
+    pop = pz.initialize(cfg, name)
+    dev = torch.device("cuda")
+    pos = torch.as_tensor(pop.positions, device=dev)
+    fit = torch.as_tensor(pop.fitness, device=dev)
+    order = torch.empty(ps, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.apo_sort_order(_lib.ptr(fit), ps, _lib.ptr(order), _lib.stream_handle()))
+    in_dr = torch.as_tensor(oracle.select_dr(13, 5, ps, 0.1).astype(np.uint8), device=dev)
+    dobj = device_objective(pz.get_objective(name), dim)
+    p_ah, f_mult, decay = iteration_scalars(4, 20)
+    pdr = p_dr_device(ps, dev)
+    idx = order.long()
+    snap_pos, snap_fit = pos.index_select(0, idx).contiguous(), fit.index_select(0, idx).contiguous()
+    outs = []
+    for ordered in (False, True):
+        out_pos, out_fit = torch.empty_like(pos), torch.empty_like(fit)
+        warn = torch.zeros(1, dtype=torch.int64, device=dev)
+        for lo, hi in ((0, 1312), (1312, 4000), (4000, ps)):
+            common = (ps, dim, 13, 5, 1, -100.0, 100.0, cfg.eps, p_ah, f_mult, decay, dobj.ref, _lib.ptr(pdr),
+                      _lib.ptr(warn), lo, hi, _lib.stream_handle())
+            if ordered:
+                _lib.check(lib.apo_run_updates_ordered(_lib.ptr(pos), _lib.ptr(fit), _lib.ptr(order), _lib.ptr(in_dr),
+                                                       _lib.ptr(out_pos), _lib.ptr(out_fit), None, None, *common))
+            else:
+                _lib.check(lib.apo_run_updates_range(_lib.ptr(snap_pos), _lib.ptr(snap_fit), _lib.ptr(in_dr),
+                                                     _lib.ptr(out_pos), _lib.ptr(out_fit), None, None, *common))
+        outs.append((out_pos.cpu().numpy(), out_fit.cpu().numpy(), int(warn.item())))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]

@@ -59,10 +59,11 @@ def assert_step_parity(sp, sf, want_pos, want_fit, want_acc, got_pos, got_fit, l
         f_cand = got_fit[k] if got_acc[k] else want_fit[k]
         assert abs(f_cand - sf[k]) <= TIE_RTOL * abs(sf[k]), \
             f"{label}: row {k} flipped with candidate {f_cand!r} vs incumbent {sf[k]!r}"
-    # flips come from clamped candidates that ARE the incumbent row (all changed dimensions pinned to a
-    # bound): the same point, evaluated once by the oracle and once by the device.  More frequent at
-    # small D, where a whole candidate is clamped more often.
-    assert flips.mean() <= 2e-3, f"{label}: {flips.sum()} accept/keep flips"
+    # flips are ties: clamped candidates that ARE the incumbent row (all changed dimensions pinned to a
+    # bound), or candidates on the same plateau of a step function (F4's non-continuous Rastrigin) --
+    # one point, evaluated once by the oracle and once by the device.  Each was asserted a tie above;
+    # this bound only catches a systematic disagreement.
+    assert flips.mean() <= 0.05, f"{label}: {flips.sum()} accept/keep flips"
     ga, wa = int(np.argmin(got_fit)), int(np.argmin(want_fit))
     if ga != wa:  # only an exact tie of the minimum may move the first index
         assert abs(got_fit[ga] - want_fit[wa]) <= TIE_RTOL * abs(want_fit[wa]), f"{label}: argmin {ga} vs {wa}"
@@ -175,5 +176,32 @@ def test_c4_basic_objective_device_loop_bit_exact(name):
         assert np.array_equal(got_pos, pos) and np.array_equal(got_fit, fit)
         f, x, row = run.best()
         assert row == int(np.argmin(fit)) and f == fit.min() and np.array_equal(x, pos[row])
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("warps", ["16", "12"])
+@pytest.mark.parametrize("fn", [6, 10])
+def test_fused_cec_kernel_teacher_forced(fn, warps, monkeypatch):
+    """The one-kernel CEC2022 update (k_update_cec, apo_update_fused.cu; opt-in with APO_CEC_FUSED=1)
+    under the same contract, at ps = 2e5, D = 100."""
+    import paper_2510_14982_b200 as pz
+
+    monkeypatch.setenv("APO_CEC_FUSED", "1")
+    monkeypatch.setenv("APO_FUSED_WARPS", warps)
+    name = f"cec2022_f{fn}"
+    ps, dim, T, seed = 200_000, 100, 25, 5
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=T, seed=seed)
+    pos, fit = oracle.initialize(seed, ps, dim, -100.0, 100.0, name)
+    run = device_run(pz, cfg, name)
+    try:
+        assert run.update_path() == "cec_fused"
+        for t in (0, 1, 20):
+            run.load(pz.Population(pos, fit, iteration=t, fe_count=ps * (t + 1)))
+            run.iterate(1)
+            got_pos, got_fit = run.population()
+            sp, sf, want_pos, want_fit, want_acc, _ = oracle_iteration(pos, fit, seed=seed, t=t, T=T, name=name)
+            assert_step_parity(sp, sf, want_pos, want_fit, want_acc, got_pos, got_fit, label=f"fused F{fn} t={t}")
+            pos, fit = want_pos, want_fit
     finally:
         run.close()

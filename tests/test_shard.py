@@ -36,6 +36,20 @@ def test_plan_partitions_whole_groups():
         assert covered == list(range(ps))
 
 
+@pytest.mark.parametrize("blocks", [2, 3, 4])
+def test_block_plan_covers_every_rank_once(blocks):
+    for ps, world in [(100, 8), (1000, 3), (1_000_000, 8), (4097, 2), (33, 2)]:
+        plan = ShardPlan(ps, world, blocks)
+        assert plan.chunk % 32 == 0 and plan.ps_pad == plan.chunk * world * blocks >= ps
+        covered = []
+        for s in range(blocks):  # block s of every rank is one contiguous span (in-place all-gather)
+            span = [plan.block(r, s) for r in range(world)]
+            for r, (lo, hi) in enumerate(span):
+                assert lo == hi or lo == (s * world + r) * plan.chunk
+            covered.extend(i for lo, hi in span for i in range(lo, hi))
+        assert sorted(covered) == list(range(ps))
+
+
 def test_key_encoding_round_trips_and_orders():
     x = np.array([-np.inf, -3.5, -1e-300, -0.0, 0.0, 1e-300, 2.0, np.inf, np.nan])
     k = encode_keys(x)
@@ -99,11 +113,11 @@ class OracleEngine:
         pass
 
 
-def _worker(rank, world, port, cfg, name, q):
+def _worker(rank, world, port, cfg, name, q, blocks=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        run = ShardedRun(cfg, name, engine=OracleEngine)
+        run = ShardedRun(cfg, name, engine=OracleEngine, blocks=blocks)
         run.initialize()
         run.iterate(cfg.max_iterations)
         pos, fit = run.population()
@@ -119,13 +133,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name,ps", [("rosenbrock", 100), ("griewank", 77)])
-def test_gloo_world2_sharded_run_equals_single_process(name, ps):
+@pytest.mark.parametrize("name,ps,blocks", [("rosenbrock", 100, 1), ("griewank", 77, None), ("sphere", 200, 3)])
+def test_gloo_world2_sharded_run_equals_single_process(name, ps, blocks):
+    """blocks = 1: one all-gather per iteration; None (default 4, capped by ps) / 3: block-interleaved
+    ranks with one asynchronous in-place all-gather per block."""
     cfg = ApoConfig(ps=ps, dim=6, bounds=Bounds(-5.0, 5.0, 6), max_iterations=12, seed=3)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, cfg, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cfg, name, q, blocks)) for r in range(2)]
     for p in procs:
         p.start()
     got = [q.get(timeout=120) for _ in procs]
@@ -148,7 +164,7 @@ def test_virtual_partitions_equal_single_gpu_and_oracle(name, ps, dim, world):
     import paper_2510_14982_b200 as pz
 
     cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=15, seed=11)
-    sh = ShardedRun(cfg, name, virtual_world=world)
+    sh = ShardedRun(cfg, name, virtual_world=world, blocks=3)
     sh.initialize()
     sh.iterate(15)
     pos, fit = sh.population()

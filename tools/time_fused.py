@@ -9,8 +9,11 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-VARIANTS = [("split", {"APO_CEC_FUSED": "0"}), ("fused16", {"APO_CEC_FUSED": "1", "APO_FUSED_WARPS": "16"}),
+VARIANTS = [("split", {"APO_CEC_FUSED": "0"}),
             ("fused12", {"APO_CEC_FUSED": "1", "APO_FUSED_WARPS": "12"})]
+if os.environ.get("TIME_VARIANTS"):  # e.g. TIME_VARIANTS='pf1:APO_CEC_PREFETCH=1;pf0:APO_CEC_PREFETCH=0'
+    VARIANTS = [(lab, dict(kv.split("=", 1) for kv in rest.split(",") if kv))
+                for lab, rest in (v.split(":", 1) for v in os.environ["TIME_VARIANTS"].split(";"))]
 
 
 def one(name, iters, skip):
