@@ -274,6 +274,8 @@ double apo_rng_uniform(int rng, uint64_t seed, uint64_t iteration, uint64_t indi
 
 /* Debug/verification entry: out[k] = device exp_glibc(x[k]). */
 int apo_debug_exp(const double *x, double *out, int64_t n, void *stream);
+/* Debug/verification entry: out[k] = device cos_glibc(x[k]) (glibc 2.39's cos, griewank). */
+int apo_debug_cos(const double *x, double *out, int64_t n, void *stream);
 
 /* Debug/verification entry: out[r] = CEC2022 basic function `basic` (ids of csrc/apo_cec.cuh /
  * oracle/cec_oracle.c; ELLIPS weights from ew, nullable) of row r of z [rows][n], evaluated by the

@@ -163,6 +163,7 @@ PROTOTYPES = {
     "apo_shard_counters": (_INT, [_P, _P, _I, C.POINTER(C.c_int64)]),
     "apo_shard_destroy": (_INT, [_P]),
     "apo_debug_exp": (_INT, [_P, _P, _I, _P]),
+    "apo_debug_cos": (_INT, [_P, _P, _I, _P]),
     "apo_debug_cec_basic": (_INT, [_INT, _P, _I, _I, _P, _P, _INT, _P]),
     "apo_philox4x32_10": (None, [_P, _P, _P]),
     "apo_rng_uniform": (_D, [_INT, _U, _U, _U, _U]),

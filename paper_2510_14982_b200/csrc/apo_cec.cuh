@@ -258,7 +258,7 @@ __device__ inline double cec_basic_warp(int b, const double* z, int n, int lane)
         double pr = 1.0;
         for (int i = lane; i < n; i += 32) {
             a += z[i] * z[i];
-            pr *= cos(z[i] / sqrt(1.0 + i));
+            pr *= cos_glibc(z[i] / sqrt(1.0 + i));  // the reference's griewank block (libm cos)
         }
         return 1.0 + wsum(a) / 4000.0 - wprod(pr);
     }
@@ -735,7 +735,7 @@ __device__ inline double cec_basic_quad_t(int b, const Zf& Z, int n, int t, cons
         double pr = 1.0;
         for (int i = t; i < n; i += 4) {
             a += Z(i) * Z(i);
-            pr *= cos(Z(i) / sqrt(1.0 + i));
+            pr *= cos_glibc(Z(i) / sqrt(1.0 + i));  // the reference's griewank block (libm cos)
         }
         return 1.0 + qsum(a) / 4000.0 - qprod(pr);
     }

@@ -298,6 +298,93 @@ __host__ __device__ __forceinline__ double exp_glibc(double x) {
     return APO_FMA(scale, tmp, scale);
 }
 
+// ---------------------------------------------------------------------------
+// cos as glibc 2.39 computes it (sysdeps/ieee754/dbl-64/s_sin.c, __cos; the x86_64 FMA variant the
+// host libm dispatches to on FMA-capable CPUs), so griewank (numba_backend.py:130, objectives.py:141)
+// matches the reference bit for bit.  Table: glibc's __sincostab (tools/gen_cos_table.py).  Range
+// reduction: |x| < 2.426 directly or from pi/2 - |x| in double-double; |x| < 105414350 by the 3-part
+// Cody-Waite split of pi/2 (reduce_sincos).  Beyond that glibc uses a multi-precision reduction
+// (__branred) that is not ported: CUDA's cos is used there (|x| >= 1e8 needs bounds far outside any
+// benchmark's).  Every multiply-add below is the fused operation GCC emits for glibc's __cos_fma.
+#include "apo_cos_glibc.h"
+__device__ const uint64_t kSinCosTab[440] = APO_SINCOS_TABLE;  // divergent indices: global (L1), not __constant__
+static const uint64_t kSinCosTabHost[440] = APO_SINCOS_TABLE;
+#ifdef __CUDA_ARCH__
+#define APO_SCTAB(i) bits_to_double(__ldg(reinterpret_cast<const unsigned long long*>(kSinCosTab) + (i)))
+#else
+#define APO_SCTAB(i) bits_to_double(kSinCosTabHost[i])
+#endif
+
+__host__ __device__ __forceinline__ double glibc_do_cos(double x, double dx) {
+    const double big = 0x1.8p45, sn3 = -0x1.5555555555515p-3, sn5 = 0x1.11110e829872fp-7, cs2 = 0.5,
+                 cs4 = -0x1.5555555555535p-5, cs6 = 0x1.6c16bedd9e239p-10;
+    if (x < 0) dx = -dx;
+    const double ux = APO_DADD(big, fabs(x));
+    x = APO_DADD(APO_DSUB(fabs(x), APO_DSUB(ux, big)), dx);
+    const double xx = APO_DMUL(x, x);
+    const double s = APO_FMA(APO_DMUL(x, xx), APO_FMA(xx, sn5, sn3), x);
+    const double c = APO_DMUL(xx, APO_FMA(xx, APO_FMA(xx, cs6, cs4), cs2));
+    const int k = (int)(uint32_t)double_to_bits(ux) << 2;
+    const double sn = APO_SCTAB(k), ssn = APO_SCTAB(k + 1), cs = APO_SCTAB(k + 2), ccs = APO_SCTAB(k + 3);
+    const double cor = APO_FMA(-sn, s, APO_FMA(-cs, c, APO_FMA(-s, ssn, ccs)));
+    return APO_DADD(cs, cor);
+}
+
+__host__ __device__ __forceinline__ double glibc_do_sin(double x, double dx) {
+    const double big = 0x1.8p45, sn3 = -0x1.5555555555515p-3, sn5 = 0x1.11110e829872fp-7, cs2 = 0.5,
+                 cs4 = -0x1.5555555555535p-5, cs6 = 0x1.6c16bedd9e239p-10;
+    const double xold = x;
+    if (fabs(x) < 0.126) {  // TAYLOR_SIN(x*x, x, dx)
+        const double s1 = -0x1.5555555555555p-3, s2 = 0x1.1111111110ecep-7, s3 = -0x1.a01a019db08b8p-13,
+                     s4 = 0x1.71de27b9a7ed9p-19, s5 = -0x1.addffc2fcdf59p-26;
+        const double xx = APO_DMUL(x, x);
+        const double p = APO_FMA(APO_FMA(APO_FMA(APO_FMA(s5, xx, s4), xx, s3), xx, s2), xx, s1);
+        const double t = APO_FMA(APO_FMA(p, x, -APO_DMUL(0.5, dx)), xx, dx);
+        return APO_DADD(x, t);
+    }
+    if (x <= 0) dx = -dx;
+    const double ux = APO_DADD(big, fabs(x));
+    x = APO_DSUB(fabs(x), APO_DSUB(ux, big));
+    const double xx = APO_DMUL(x, x);
+    const double s = APO_DADD(x, APO_FMA(APO_DMUL(x, xx), APO_FMA(xx, sn5, sn3), dx));
+    const double c = APO_FMA(x, dx, APO_DMUL(xx, APO_FMA(xx, APO_FMA(xx, cs6, cs4), cs2)));
+    const int k = (int)(uint32_t)double_to_bits(ux) << 2;
+    const double sn = APO_SCTAB(k), ssn = APO_SCTAB(k + 1), cs = APO_SCTAB(k + 2), ccs = APO_SCTAB(k + 3);
+    const double cor = APO_FMA(cs, s, APO_FMA(-sn, c, APO_FMA(s, ccs, ssn)));
+    return copysign(APO_DADD(sn, cor), xold);
+}
+
+__host__ __device__ __forceinline__ double cos_glibc(double x) {
+    const uint32_t k = (uint32_t)(double_to_bits(x) >> 32) & 0x7fffffffu;
+    if (k < 0x3e400000u) return 1.0;                      // |x| < 2^-27
+    if (k < 0x3feb6000u) return glibc_do_cos(x, 0.0);    // |x| < 0.855469
+    if (k < 0x400368fdu) {                                // |x| < 2.426265: cos x = sin(pi/2 - |x|)
+        const double hp0 = 0x1.921fb54442d18p0, hp1 = 0x1.1a62633145c07p-54;
+        const double y = APO_DSUB(hp0, fabs(x));
+        const double a = APO_DADD(y, hp1);
+        return glibc_do_sin(a, APO_DADD(APO_DSUB(y, a), hp1));
+    }
+    if (k < 0x419921fbu) {                                // |x| < 105414350: reduce_sincos
+        const double hpinv = 0x1.45f306dc9c883p-1, toint = 0x1.8p52, mp1 = 0x1.921fb58p0,
+                     mp2 = -0x1.dde973cp-27, pp3 = -0x1.cb3b398p-55, pp4 = -0x1.d747f23e32ed7p-83;
+        const double t = APO_FMA(x, hpinv, toint);
+        const double xn = APO_DSUB(t, toint);
+        const double y = APO_FMA(-xn, mp2, APO_FMA(-xn, mp1, x));
+        int n = (int)((uint32_t)double_to_bits(t) & 3u);
+        double t1 = APO_DMUL(xn, pp3);
+        const double t2 = APO_DSUB(y, t1);
+        double db = APO_DSUB(APO_DSUB(y, t2), t1);
+        t1 = APO_DMUL(xn, pp4);
+        const double b = APO_DSUB(t2, t1);
+        db = APO_DADD(db, APO_DSUB(APO_DSUB(t2, b), t1));
+        n += 1;
+        const double r = (n & 1) ? glibc_do_cos(b, db) : glibc_do_sin(b, db);
+        return (n & 2) ? -r : r;
+    }
+    if (k < 0x7ff00000u) return cos(x);  // __branred range: not ported (see above)
+    return x - x;                        // inf, nan -> nan
+}
+
 // Neighbour influence weight exp(-|fa/(fb+eps)|): core.py:253-255.
 __host__ __device__ __forceinline__ double rank_weight(double fa, double fb, double eps) {
     return exp_glibc(-fabs(APO_DDIV(fa, APO_DADD(fb, eps))));

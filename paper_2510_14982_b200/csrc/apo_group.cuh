@@ -430,7 +430,7 @@ __device__ __forceinline__ void write_terms(const ObjDesc& O, double* T1, double
         break;
     case OBJ_GRIEWANK:
         T1[d] = c * c;
-        T2[d] = cos(c / sqrt((double)d + 1.0));
+        T2[d] = cos_glibc(c / sqrt((double)d + 1.0));  // glibc-exact (numba_backend.py:130)
         break;
     default:
         if (O.code >= OBJ_CEC_BASE || O.code == OBJ_OTSU_ML || O.code == OBJ_KAPUR_ML) {

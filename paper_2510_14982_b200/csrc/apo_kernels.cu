@@ -303,6 +303,11 @@ __global__ void k_threshold_tables(const long long* __restrict__ counts, int met
     }
 }
 
+__global__ void k_debug_cos(const double* x, double* out, long long n) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        out[k] = cos_glibc(x[k]);
+}
+
 __global__ void k_debug_exp(const double* x, double* out, long long n) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
         out[k] = exp_glibc(x[k]);
@@ -854,6 +859,14 @@ void apo_philox4x32_10(const uint32_t* ctr4, const uint32_t* key2, uint32_t* out
 
 double apo_rng_uniform(int rng, uint64_t seed, uint64_t iteration, uint64_t individual, uint64_t counter) {
     return uniform(stream_key(rng, seed, iteration, individual), counter);
+}
+
+int apo_debug_cos(const double* x, double* out, int64_t n, void* stream) {
+    APO_CHECK(n >= 0, "bad n");
+    if (n == 0) return APO_OK;
+    k_debug_cos<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(x, out, n);
+    APO_CUDA(cudaGetLastError());
+    return APO_OK;
 }
 
 int apo_debug_exp(const double* x, double* out, int64_t n, void* stream) {

@@ -136,9 +136,8 @@ __device__ inline double eval_warp(const ObjDesc& O, const double* c, double* t,
         if (lane == 0) f = seq_sum(t, 0, dim - 1);
         break;
     case OBJ_GRIEWANK:
-        // cos through CUDA's libdevice (<= 1-2 ulp); glibc's cos is not
-        // ported, so griewank agrees to ~1e-15 relative, not bit for bit.
-        for (int d = lane; d < dim; d += 32) t[d] = cos(c[d] / sqrt((double)d + 1.0));
+        // glibc's cos (cos_glibc, apo_device.cuh): bit for bit with numba_backend.py:130
+        for (int d = lane; d < dim; d += 32) t[d] = cos_glibc(c[d] / sqrt((double)d + 1.0));
         __syncwarp();
         if (lane == 0) {
             double s = 0.0, p = 1.0;

@@ -152,6 +152,21 @@ def initialize(cfg: ApoConfig, objective) -> Population:
 
 STEP_CHUNK_MIN_PS = 1 << 16  # step(): overlap the result's D2H with the update from this size on
 
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev):
+    """One long-lived side stream per device for step()'s copies: torch's caching allocator keeps blocks
+    per stream, so a fresh stream each call would strand the 800 MB row buffer of the last call and
+    allocate a new one (cudaMalloc/cudaFree spikes of 100-200 ms)."""
+    import torch
+
+    key = str(dev)
+    st = _COPY_STREAMS.get(key)
+    if st is None:
+        st = _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return st
+
 
 def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: EngineMode = None,
          backend: Optional[str] = None) -> Population:
@@ -177,7 +192,7 @@ def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: Engin
     # stream in on a second stream
     fit = _to_device(pop.fitness, dev)
     if lean:
-        copy = torch.cuda.Stream(device=dev)
+        copy = _copy_stream(dev)
         with torch.cuda.stream(copy):
             pos = _to_device(pop.positions, dev)
         pos.record_stream(main)

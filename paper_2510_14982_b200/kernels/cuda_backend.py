@@ -96,8 +96,10 @@ def run_updates_to_host(pos, fit, in_dr, cfg: ApoConfig, objective: Objective, i
     p_ah, f_mult, decay = iteration_scalars(iteration, cfg.max_iterations)
     dobj = device_objective(objective, dim)
     pdr = p_dr_device(ps, dev)
+    from ..engine import _copy_stream
+
     compute = torch.cuda.current_stream()
-    copy = torch.cuda.Stream(device=dev)
+    copy = _copy_stream(dev)
     step = -(-ps // chunks)
     step = (step + 31) // 32 * 32
     for lo in range(0, ps, step):

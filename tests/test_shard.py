@@ -254,8 +254,6 @@ def test_run_many_single_process_equals_oracle():
     seeds = [s for _ in RUN_MANY_NAMES for s in RUN_MANY_SEEDS]
     res = run_many(cfg, names, seeds, want_trace=True)
     want = oracle_batch(cfg, [pz.get_objective(n) for n in names], seeds, want_trace=True)
-    exact = np.array([n != "griewank" for n in names])  # griewank's cos is CUDA's
-    assert np.array_equal(res.best_fitness[exact], want.best_fitness[exact])
-    assert np.array_equal(res.best_position[exact], want.best_position[exact])
-    assert np.array_equal(res.trace[exact], want.trace[exact]) and np.array_equal(res.warnings, want.warnings)
-    np.testing.assert_allclose(res.trace[~exact], want.trace[~exact], rtol=1e-9)
+    assert np.array_equal(res.best_fitness, want.best_fitness)
+    assert np.array_equal(res.best_position, want.best_position)
+    assert np.array_equal(res.trace, want.trace) and np.array_equal(res.warnings, want.warnings)
