@@ -30,7 +30,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-
 SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_batch.cu", "apo_batch_m1.cu",
            "apo_batch_m2.cu", "apo_batch_m4.cu", "apo_batch_m0.cu", "apo_batch_warp.cu", "apo_cec_eval.cu",
            "apo_cec_gemm.cu", "apo_prologue.cu", "apo_update_fused.cu",
-           "apo_update_fused12.cu", "apo_update_fused_ws.cu"]
+           "apo_update_fused12.cu"]
 
 # CEC2022-only TUs (parity unpinned, checked at 1e-9 relative): FMA contraction allowed.  Every TU
 # on the reference's bit-exact path keeps --fmad=false.

@@ -117,6 +117,18 @@ def runs_csv(records) -> str:
                  for r in records for p in r["per_run"]], RUN_COLUMNS)
 
 
+def modes_for(engine: str, workers) -> list:
+    """cli.py:153-159: seq and/or par (par with --workers, default "auto")."""
+    import paper_2510_14982_b200 as pz
+
+    modes = []
+    if engine in ("seq", "both"):
+        modes.append(pz.EngineMode.sequential())
+    if engine in ("par", "both"):
+        modes.append(pz.EngineMode.parallel(workers if workers is not None else "auto"))
+    return modes
+
+
 def cmd_bench(args) -> int:
     import paper_2510_14982_b200 as pz
 
@@ -125,11 +137,7 @@ def cmd_bench(args) -> int:
         raise ValueError(f"--lower must be below --upper, got [{args.lower}, {args.upper}]")
     cfg = pz.ApoConfig(ps=args.ps, dim=args.dim, bounds=pz.Bounds(args.lower, args.upper, args.dim),
                        max_iterations=args.iters, seed=seed, rng=args.rng)
-    modes = []
-    if args.engine in ("seq", "both"):
-        modes.append(pz.EngineMode.sequential())
-    if args.engine in ("par", "both"):
-        modes.append(pz.EngineMode.parallel("auto"))
+    modes = modes_for(args.engine, args.workers)
     result = pz.benchmark(cfg, args.function, args.runs, modes=modes)
     records = bench_records(result, args.ps, args.dim, args.iters, seed)
     fmt = args.format or ("json" if args.out and str(args.out).endswith(".json") else "csv")
@@ -248,12 +256,40 @@ def cmd_threshold(args) -> int:
     except Exception as exc:
         raise ImageError(f"{args.image}: {exc}") from None
     seed = resolve_seed(args.seed)
-    if args.levels == 1 and args.method == "otsu":
-        res = pz.apo_threshold(pz.GrayImage(img), ps=args.ps, iterations=args.iters, seed=seed)
-        print(f"threshold={res.threshold} variance={format_number(res.variance)}")
-    else:
+    if not (args.levels == 1 and args.method == "otsu"):  # multilevel: no reference counterpart
         res = pz.apo_multithreshold(img, args.levels, args.method, ps=args.ps, iterations=args.iters, seed=seed)
         print(f"thresholds={','.join(str(t) for t in res.thresholds)} {args.method}={format_number(res.value)}")
+        return 0
+    # the reference's threshold command (cli.py:262-303): --runs seeds per mode, per-run lines, averages,
+    # optional binarised output of the last run and the exhaustive-search oracle check (exit 1 on mismatch)
+    from statistics import fmean
+
+    from . import imaging
+
+    gray = pz.GrayImage(img)
+    oracle = imaging.brute_force_otsu(imaging.histogram(gray)) if args.check_oracle else None
+    mismatches, last = 0, None
+    for mode in modes_for(args.engine, args.workers):
+        thresholds, seconds = [], []
+        for r in range(args.runs):
+            res = pz.apo_threshold(gray, ps=args.ps, iterations=args.iters, seed=seed + r, mode=mode)
+            thresholds.append(res.threshold)
+            seconds.append(res.run.wall_clock_seconds)
+            last = res
+            print(f"{mode.kind} run {r + 1}: seed={seed + r} threshold={res.threshold} "
+                  f"variance={format_number(res.variance)} seconds={format_number(res.run.wall_clock_seconds)}")
+            if oracle is not None and res.variance != oracle[1]:
+                mismatches += 1
+                print(f"oracle mismatch: {mode.kind} run {r + 1} reached {res.variance!r}, "
+                      f"exhaustive search reaches {oracle[1]!r} at t={oracle[0]}", file=sys.stderr)
+        print(f"{mode.kind} Avg. Best Th. {fmean(thresholds):.2f}  Avg. Time (s) {format_number(fmean(seconds))}")
+    if args.emit is not None and last is not None:
+        black_white = imaging.apply_threshold(gray, last.threshold)
+        atomic_write(args.emit, imaging.write_pgm(black_white, binary=args.emit_format == "p5"))
+    if oracle is not None:
+        if mismatches:
+            return 1
+        print(f"oracle check: ok (t={oracle[0]}, variance={format_number(oracle[1])})")
     return 0
 
 
@@ -271,6 +307,19 @@ def _int_at_least(lo):
         return v
 
     return parse
+
+
+def _workers(text):
+    """cli.py:110-119: a worker count >= 1 or "auto"."""
+    if text == "auto":
+        return "auto"
+    try:
+        v = int(text)
+    except ValueError:
+        raise argparse.ArgumentTypeError(f"expected a worker count or 'auto', got {text!r}") from None
+    if v < 1:
+        raise argparse.ArgumentTypeError(f"worker count must be >= 1, got {v}")
+    return v
 
 
 def _seed(text):
@@ -291,6 +340,7 @@ def build_parser() -> argparse.ArgumentParser:
     b.add_argument("--runs", type=_int_at_least(1), default=5)
     b.add_argument("--seed", type=_seed, default=None)
     b.add_argument("--engine", choices=("seq", "par", "both"), default="both")
+    b.add_argument("--workers", type=_workers, default=None)
     b.add_argument("--rng", choices=("keyed", "philox"), default="keyed")
     b.add_argument("--lower", type=float, default=-100.0)
     b.add_argument("--upper", type=float, default=100.0)
@@ -304,6 +354,13 @@ def build_parser() -> argparse.ArgumentParser:
     t.add_argument("--ps", type=_int_at_least(1), default=100)
     t.add_argument("--iters", type=_int_at_least(0), default=50)
     t.add_argument("--seed", type=_seed, default=None)
+    t.add_argument("--runs", type=_int_at_least(1), default=5)
+    t.add_argument("--engine", choices=("seq", "par", "both"), default="seq")
+    t.add_argument("--workers", type=_workers, default=None)
+    t.add_argument("--emit", default=None, help="write the binarized last run here")
+    t.add_argument("--emit-format", choices=("p5", "p2"), default="p5")
+    t.add_argument("--check-oracle", action="store_true",
+                   help="compare every run with the exhaustive search; exit 1 on a mismatch")
     t.set_defaults(handler=cmd_threshold)
     r = sub.add_parser("report", help="join sequential/parallel bench records into a speedup table")
     r.add_argument("--in", dest="inputs", nargs="+", required=True)

@@ -332,19 +332,16 @@ int launch_cec_eval(bool sel_mode, const UpdArgs& a, cudaStream_t st, uint8_t* c
 
 // Which kernels an update launch runs (apo_run_update_path): 0 one fused kernel (basic objectives,
 // or CEC2022 without DMMA tables), 1 CEC2022 split (k_update_group candidates + k_cec_eval), 2 fused
-// CEC2022 (k_update_cec), 3 CEC2022 GEMM (candidates + k_dgemm_nn + k_cec_finish), 4 fused CEC2022,
-// warp-specialised (k_update_cec_ws).
+// CEC2022 (k_update_cec), 3 CEC2022 GEMM (candidates + k_dgemm_nn + k_cec_finish).
 int update_path(bool sel_mode, const UpdArgs& a, bool have_cand_ok, bool have_counter) {
     const int dim = a.P.dim;
     const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
     const bool cec = have_cand_ok && a.O.code > APO_OBJ_CEC2022_BASE;
     if (cec && dim <= kGroupMaxDim && dim <= kCecEvalMaxDim && a.O.cec.rot_pad != nullptr) {
-        // APO_CEC_FUSED: 0 split (two kernels), 1 one kernel, 2 one warp-specialised kernel
+        // APO_CEC_FUSED: 0 split (two kernels, the default: measured faster), 1 one kernel
         const int env_fused = getenv("APO_CEC_FUSED") ? atoi(getenv("APO_CEC_FUSED")) : 0;
         size_t fsmem = 0;
         int fss = 0;
-        if (sel_mode && env_fused == 2 && have_counter && ws_shape(a, smem_optin(), ws_producers(), &fsmem, &fss) >= 2)
-            return 4;
         if (sel_mode && env_fused == 1 && have_counter && fused_cec_shape(a, smem_optin(), &fsmem, &fss) > 0) return 2;
         return 1;
     }
@@ -369,10 +366,9 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     }
     // SEL rows (device loop): candidates, DMMA evaluation and select as one kernel (apo_update_fused.cu)
     const int path = split ? update_path(sel_mode, a, true, tile_counter != nullptr) : 0;
-    if (path == 2 || path == 4) {
+    if (path == 2) {
         if (a.rank_hi <= 0) a.rank_hi = a.P.ps;
-        if (path == 2) APO_CUDA(launch_update_cec_fused(a, st, tile_counter, smem_optin(), num_sms()));
-        else APO_CUDA(launch_update_cec_ws(a, st, tile_counter, smem_optin(), num_sms()));
+        APO_CUDA(launch_update_cec_fused(a, st, tile_counter, smem_optin(), num_sms()));
         if (mid_event) APO_CUDA(cudaEventRecord(mid_event, st));
         return APO_OK;
     }

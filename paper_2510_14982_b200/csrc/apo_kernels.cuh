@@ -702,9 +702,5 @@ cudaError_t launch_debug_cec_basic(int b, const double* z, long long rows, int n
 // apo_update_fused.cu: CEC2022 (D <= 104, SEL rows) candidates + DMMA evaluation + select in one kernel
 int fused_cec_shape(const UpdArgs& a, int optin, size_t* smem, int* stage_shift);
 cudaError_t launch_update_cec_fused(const UpdArgs& a, cudaStream_t st, unsigned* counter, int optin, int num_sms);
-// apo_update_fused_ws.cu: the warp-specialised form (producer warps -> X-tile ring -> DMMA consumer warps)
-int ws_shape(const UpdArgs& a, int optin, int np, size_t* smem, int* stage_shift);
-int ws_producers();
-cudaError_t launch_update_cec_ws(const UpdArgs& a, cudaStream_t st, unsigned* counter, int optin, int num_sms);
 
 }  // namespace apo

@@ -90,3 +90,40 @@ def test_bench_and_threshold_commands(tmp_path, capsys):
     np.save(tmp_path / "img.npy", img)
     assert cli.main(["threshold", "--image", str(tmp_path / "img.npy"), "--levels", "2", "--method", "kapur"]) == 0
     assert capsys.readouterr().out.startswith("thresholds=")
+
+
+def _strip_seconds(lines):
+    import re
+
+    return [re.sub(r"(seconds=|Avg\. Time \(s\) )\S+", r"\1<t>", ln) for ln in lines]
+
+
+@pytest.mark.gpu
+def test_threshold_command_matches_reference_cli(tmp_path, capsys):
+    """`threshold --runs --engine both --check-oracle --emit` prints the reference CLI's lines
+    (cli.py:262-303: per-run seed/threshold/variance, per-mode averages, the oracle check) and writes the
+    same binarised PGM; only the seconds differ.  The reference (baseline/_ref, numba) runs beside it."""
+    import sys
+
+    ref_site = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_site, "protozoa")):
+        pytest.skip("reference not installed in baseline/_ref")
+    rnd = np.random.default_rng(3)
+    img = np.clip(np.where(rnd.random((96, 80)) < 0.4, rnd.normal(70, 12, (96, 80)),
+                           rnd.normal(190, 14, (96, 80))), 0, 255).astype(np.uint8)
+    pgm = tmp_path / "img.pgm"
+    pgm.write_bytes(b"P5\n80 96\n255\n" + img.tobytes())
+    args = ["threshold", "--image", str(pgm), "--runs", "3", "--engine", "both", "--seed", "5", "--check-oracle",
+            "--emit-format", "p2"]
+    assert cli.main(args + ["--emit", str(tmp_path / "ours.pgm")]) == 0
+    ours = capsys.readouterr().out.splitlines()
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_cli")
+    sys.path.insert(0, ref_site)
+    try:
+        from protozoa import cli as ref_cli
+    finally:
+        sys.path.remove(ref_site)
+    assert ref_cli.main(args + ["--emit", str(tmp_path / "ref.pgm")]) == 0
+    ref = capsys.readouterr().out.splitlines()
+    assert _strip_seconds(ours) == _strip_seconds(ref)
+    assert (tmp_path / "ours.pgm").read_bytes() == (tmp_path / "ref.pgm").read_bytes()
