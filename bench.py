@@ -320,6 +320,14 @@ def c4_measure(args, name, rank, world, local, K, W):
         kernels = [hbm_entry("k_update_group<SEL> (candidates only)", cand_ms, f"c4:{name}"),
                    dmma_entry("k_cec_eval (DMMA f64 m8n8k4 rotation + basic + greedy select)", eval_ms,
                               f"c4eval:{name}", {"also_reads_bytes_per_eval": 8 * dim + 16})]
+    elif path == "basic_split":
+        # candidates (HBM-bound) + lane-per-protozoon sequential evaluation: the update as a whole against
+        # the HBM roof (the evaluation re-reads the 8 D bytes per candidate: reported beside it)
+        e = hbm_entry("k_update_group<SEL> (candidates) + k_basic_eval (sequential fold + select)", cand_ms + eval_ms,
+                      f"c4:{name}")
+        e["split_ms"] = {"candidates": round(cand_ms / n, 4), "evaluate": round(eval_ms / n, 4)}
+        e["eval_reread_bytes_per_eval"] = 8 * dim + 16
+        kernels = [e]
     else:
         kernels = [hbm_entry("k_update_group<SEL> (fused update, " + path + ")", cand_ms + eval_ms, f"c4:{name}")]
     dominant = max(kernels, key=lambda k: k["kernel_ms_avg"])

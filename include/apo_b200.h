@@ -203,7 +203,9 @@ int apo_run_profile_read(apo_run *run, double *update_ms_host, int64_t *launches
 int apo_run_profile_split(apo_run *run, double *candidates_ms_host, double *evaluate_ms_host, int64_t *launches_host);
 /* Which kernels one iteration's update runs: 0 one fused kernel (basic objectives), 1 CEC2022 split
  * (candidates, then the DMMA evaluation kernel), 2 CEC2022 fused (one kernel: candidates + DMMA
- * evaluation + select; opt-in APO_CEC_FUSED=1), 3 CEC2022 at D > 104 (candidates, DMMA GEMM, finish). */
+ * evaluation + select; opt-in APO_CEC_FUSED=1), 3 CEC2022 at D > 104 (candidates, DMMA GEMM, finish),
+ * 4 the reference's six objectives at 33 <= D <= 256 (candidates, then a lane-per-protozoon sequential
+ * evaluation + select). */
 int apo_run_update_path(apo_run *run, int *path_host);
 
 /*

@@ -332,7 +332,8 @@ int launch_cec_eval(bool sel_mode, const UpdArgs& a, cudaStream_t st, uint8_t* c
 
 // Which kernels an update launch runs (apo_run_update_path): 0 one fused kernel (basic objectives,
 // or CEC2022 without DMMA tables), 1 CEC2022 split (k_update_group candidates + k_cec_eval), 2 fused
-// CEC2022 (k_update_cec), 3 CEC2022 GEMM (candidates + k_dgemm_nn + k_cec_finish).
+// CEC2022 (k_update_cec), 3 CEC2022 GEMM (candidates + k_dgemm_nn + k_cec_finish), 4 the reference's
+// objectives split (candidates + k_basic_eval).
 int update_path(bool sel_mode, const UpdArgs& a, bool have_cand_ok, bool have_counter) {
     const int dim = a.P.dim;
     const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
@@ -346,6 +347,8 @@ int update_path(bool sel_mode, const UpdArgs& a, bool have_cand_ok, bool have_co
         return 1;
     }
     if (cec && dim > kCecEvalMaxDim && a.O.cec.rot_gemm != nullptr && (fn_id <= 8 || fn_id == 10)) return 3;
+    const int bs = getenv("APO_BASIC_SPLIT_MIN_DIM") ? atoi(getenv("APO_BASIC_SPLIT_MIN_DIM")) : 33;
+    if (have_cand_ok && basic_split_code(a.O.code) && bs > 0 && dim >= bs && dim <= kGroupMaxDim) return 4;
     return 0;
 }
 
@@ -360,7 +363,9 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     // D > 104: candidates, then the rotation of every candidate as one DMMA GEMM (apo_cec_gemm.cu)
     const bool gemm = !split && cand_ok && a.O.code > APO_OBJ_CEC2022_BASE && dim > kCecEvalMaxDim &&
                       a.O.cec.rot_gemm != nullptr && (fn_id <= 8 || fn_id == 10);
-    if (split || gemm) {
+    // the reference's objectives at D > 32: candidates, then lane-per-protozoon evaluation (k_basic_eval)
+    const bool bsplit = group && cand_ok && update_path(sel_mode, a, true, true) == 4;
+    if (split || gemm || bsplit) {
         a.cand_ok = cand_ok;
         a.cec_bufs = 0;
     }
@@ -378,7 +383,8 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     while (w > 1 && per_warp * (size_t)w + 1024 > (size_t)smem_optin()) w--;  // e.g. fused CEC at D ~ 150-256
     const size_t smem = per_warp * (size_t)w;
     const bool cec = a.O.code > APO_OBJ_CEC2022_BASE;
-    const void* fn = sel_mode ? pick_update_sel(dim, split || gemm, cec) : pick_update_dense(dim, split || gemm, cec);
+    const void* fn = sel_mode ? pick_update_sel(dim, split || gemm || bsplit, cec)
+                              : pick_update_dense(dim, split || gemm || bsplit, cec);
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
@@ -402,6 +408,40 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         APO_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(32 * w), args, smem, st));
     }
     if (mid_event) APO_CUDA(cudaEventRecord(mid_event, st));
+    if (bsplit) {
+        BasicEvalArgs B{};
+        B.n_rows = a.rank_hi - a.rank_lo;
+        B.row0 = a.rank_lo;
+        B.dim = dim;
+        B.ld = a.P.ld;
+        B.order = sel_mode ? nullptr : a.order;
+        B.O = a.O;
+        B.pos0 = a.pos0;
+        B.pos1 = a.pos1;
+        B.sel = a.sel;
+        B.sel_next = a.sel_next;
+        B.pos = a.pos;
+        B.out_pos = a.out_pos;
+        B.out_acc = a.out_acc;
+        B.out_warn = a.out_warn;
+        B.fit = a.fit;
+        B.out_fit = a.out_fit;
+        B.cand_ok = cand_ok;
+        B.warn_count = a.warn_count;
+        B.trace_key = a.trace_key;
+        const void* fb = sel_mode ? (const void*)k_basic_eval<true> : (const void*)k_basic_eval<false>;
+        if (int rc = set_smem(fb, kBasicEvalSmem)) return rc;
+        int bper = 1;
+        APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bper, fb, 32 * kBasicEvalWarps, kBasicEvalSmem));
+        if (bper < 1) bper = 1;
+        const long long groups = ((long long)B.n_rows + 31) / 32;
+        const long long bneed = (groups + kBasicEvalWarps - 1) / kBasicEvalWarps;
+        const long long bcap = (long long)bper * num_sms();
+        void* bargs[] = {(void*)&B};
+        APO_CUDA(cudaLaunchKernel(fb, dim3((unsigned)(bneed < bcap ? bneed : bcap)), dim3(32 * kBasicEvalWarps), bargs,
+                                  kBasicEvalSmem, st));
+        return APO_OK;
+    }
     if (gemm) {
         CecGemmArgs G{};
         G.row0 = a.rank_lo;
@@ -708,7 +748,8 @@ int updates_range(const double* positions, const double* fitness, const int32_t*
     A.order = order;  // rows of positions/fitness read at order[rank]; outputs by rank
     A.cec_bufs = cec_bufs_for(A.O.code);
     uint8_t* cand_ok = nullptr;
-    const bool cec = A.O.code > APO_OBJ_CEC2022_BASE;
+    // CEC2022 and the split basic objectives need the per-row candidate finiteness scratch
+    const bool cec = A.O.code > APO_OBJ_CEC2022_BASE || basic_split_code(A.O.code);
     const size_t ok_bytes = ((size_t)ps + 15) & ~(size_t)15;  // cand_ok, then the k_cec_eval tile counter
     if (cec) APO_CUDA(cudaMallocAsync((void**)&cand_ok, ok_bytes + 16, as_stream(stream)));
     unsigned* counter = cec ? reinterpret_cast<unsigned*>(cand_ok + ok_bytes) : nullptr;

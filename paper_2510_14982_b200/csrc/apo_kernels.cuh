@@ -662,6 +662,149 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
     block_finish(my_min, my_warn, A.warn_count, A.trace_key);
 }
 
+// ---------------------------------------------------------------------------
+// The reference's six objectives on an HBM-resident population, split like CEC2022: k_update_group
+// <KIND_CAND> writes candidates (+ a finiteness flag), then k_basic_eval evaluates them LANE PER
+// PROTOZOON -- the reference's sequential left-to-right loop (numba_backend.py:93-131) run by one lane
+// over its own candidate, bit for bit -- and applies the greedy select (numba_backend.py:270-290).
+// The fused group kernel instead folds each protozoon's terms with 1 of 32 lanes while the warp waits;
+// here a warp transposes 32 candidate rows through shared memory in 32 x 32 blocks (coalesced row
+// reads, conflict-free column reads: stride 33) and all 32 lanes fold at once.
+struct BasicEvalArgs {
+    int n_rows, dim, ld;
+    int row0;          // first row (dense: rank) of the range
+    const int* order;  // dense + order: old row/fitness of rank r at order[r] (nullable)
+    ObjDesc O;
+    const double* pos0;  // SEL: candidate of slot r in its alternate buffer
+    const double* pos1;
+    const uint8_t* sel;
+    uint8_t* sel_next;
+    const double* pos;  // dense: old rows
+    double* out_pos;    // dense: candidates in, kept rows out
+    uint8_t* out_acc;
+    uint8_t* out_warn;
+    const double* fit;
+    double* out_fit;
+    const uint8_t* cand_ok;
+    unsigned long long* warn_count;
+    unsigned long long* trace_key;
+};
+
+__host__ __device__ inline bool basic_split_code(int code) { return code >= OBJ_SPHERE && code <= OBJ_GRIEWANK; }
+
+constexpr int kBasicEvalWarps = 8;
+constexpr size_t kBasicEvalSmem = (size_t)kBasicEvalWarps * 32 * 33 * 8;  // one 32 x 33 block per warp
+
+template <bool SEL>
+__global__ void __launch_bounds__(32 * kBasicEvalWarps) k_basic_eval(BasicEvalArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    double(*T)[33] = reinterpret_cast<double(*)[33]>(smem) + (size_t)warp * 32;
+    const int dim = A.dim, code = A.O.code;
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    const int ngroups = (A.n_rows + 31) / 32;
+    for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
+        const int g0 = A.row0 + grp * 32;
+        const int nb = min(32, A.row0 + A.n_rows - g0);
+        const int r = g0 + lane;  // this lane's row
+        const bool live = lane < nb;
+        uint8_t cur = 0;
+        if constexpr (SEL) cur = live ? A.sel[r] : 0;
+        // running state of the reference's loop (numba_backend.py:96-131)
+        double s = 0.0, s2 = 0.0, p = 1.0, first = 0.0, prev = 0.0;
+        for (int d0 = 0; d0 < dim; d0 += 32) {
+            const int w = min(32, dim - d0);
+            for (int j = 0; j < nb; j++) {  // row g0 + j, columns d0 .. d0 + w: one coalesced read
+                const int rj = g0 + j;
+                const double* src;
+                if constexpr (SEL) {
+                    const uint8_t sj = __shfl_sync(kFull, cur, j);
+                    src = (sj ? A.pos0 : A.pos1) + (size_t)rj * A.ld;  // the alternate buffer
+                } else {
+                    src = A.out_pos + (size_t)rj * A.ld;
+                }
+                if (lane < w) T[j][lane] = src[d0 + lane];
+            }
+            __syncwarp();
+            if (live) {
+                for (int k = 0; k < w; k++) {
+                    const int d = d0 + k;
+                    const double c = T[lane][k];
+                    switch (code) {
+                    case OBJ_SPHERE: s += c * c; break;
+                    case OBJ_BENT_CIGAR:
+                        if (d == 0) first = c * c;
+                        else s += c * c;
+                        break;
+                    case OBJ_ELLIPTIC: s += (A.O.table[d] * c) * c; break;
+                    case OBJ_HGBAT:
+                        s += c;
+                        s2 += c * c;
+                        break;
+                    case OBJ_ROSENBROCK:
+                        if (d >= 1) {
+                            const double a = c - prev * prev;
+                            const double b = prev - 1.0;
+                            s += 100.0 * (a * a) + b * b;
+                        }
+                        prev = c;
+                        break;
+                    default:  // OBJ_GRIEWANK
+                        s += c * c;
+                        p *= cos_glibc(c / sqrt((double)d + 1.0));
+                        break;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        double nf = 0.0;
+        switch (code) {
+        case OBJ_SPHERE:
+        case OBJ_ELLIPTIC:
+        case OBJ_ROSENBROCK: nf = s; break;
+        case OBJ_BENT_CIGAR: nf = first + 1e6 * s; break;
+        case OBJ_HGBAT: nf = sqrt(fabs(s2 * s2 - s * s)) + (0.5 * s2 + s) / (double)dim + 0.5; break;
+        default: nf = 1.0 + s / 4000.0 - p; break;
+        }
+        bool acc = false;
+        if (live) {
+            const double fit_i = A.fit[(!SEL && A.order) ? A.order[r] : r];
+            double kept = fit_i;
+            bool warned = false;
+            if (A.cand_ok[r] && isfinite(nf)) {
+                acc = nf < fit_i;
+                if (acc) kept = nf;
+            } else {
+                warned = true;
+            }
+            A.out_fit[r] = kept;
+            if constexpr (SEL) {
+                A.sel_next[r] = acc ? (uint8_t)(cur ^ 1) : cur;
+            } else {
+                if (A.out_acc) A.out_acc[r] = acc ? 1 : 0;
+                if (A.out_warn) A.out_warn[r] = warned ? 1 : 0;
+            }
+            const unsigned long long k = sort_key(kept);
+            my_min = k < my_min ? k : my_min;
+            my_warn += warned ? 1u : 0u;
+        }
+        if constexpr (!SEL) {  // rejected rows get the old row back (numba_backend.py:286-288)
+            unsigned rej = __ballot_sync(kFull, live && !acc);
+            while (rej) {
+                const int j = __ffs(rej) - 1;
+                rej &= rej - 1;
+                const int old_row = A.order ? A.order[g0 + j] : g0 + j;
+                const double* x = A.pos + (size_t)old_row * A.ld;
+                double* dst = A.out_pos + (size_t)(g0 + j) * A.ld;
+                for (int d = lane; d < dim; d += 32) dst[d] = x[d];
+            }
+        }
+    }
+    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
+}
+
 // CEC2022 at D > kCecEvalMaxDim: transform -> DMMA GEMM -> finish (apo_cec_gemm.cu).
 struct CecGemmArgs {
     int n_rows, row0, dim, ld, kp, np, comp;

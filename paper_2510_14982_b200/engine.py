@@ -314,11 +314,11 @@ class DeviceRun:
         return a.value, b.value, n.value
 
     def update_path(self) -> str:
-        """Kernels of one iteration's update: "fused" (basic objectives), "cec_split", "cec_fused", "cec_gemm"
-        (apo_run_update_path)."""
+        """Kernels of one iteration's update: "fused" (one kernel), "cec_split", "cec_fused", "cec_gemm",
+        "basic_split" (apo_run_update_path)."""
         p = C.c_int()
         _lib.check(self.lib.apo_run_update_path(self.handle, C.byref(p)), "apo_run_update_path")
-        return ("fused", "cec_split", "cec_fused", "cec_gemm")[p.value]
+        return ("fused", "cec_split", "cec_fused", "cec_gemm", "basic_split")[p.value]
 
     def close(self):
         if self.handle:
