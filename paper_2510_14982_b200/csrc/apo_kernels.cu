@@ -429,17 +429,21 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         B.cand_ok = cand_ok;
         B.warn_count = a.warn_count;
         B.trace_key = a.trace_key;
-        const void* fb = sel_mode ? (const void*)k_basic_eval<true> : (const void*)k_basic_eval<false>;
-        if (int rc = set_smem(fb, kBasicEvalSmem)) return rc;
+        // whole rows by TMA when they are 16-byte multiples and small enough, else 32 x 32 cp.async blocks
+        const bool tma = (B.ld % 2) == 0 && dim <= kBasicTmaMaxDim;
+        const void* fb = tma ? (sel_mode ? (const void*)k_basic_eval_tma<true> : (const void*)k_basic_eval_tma<false>)
+                             : (sel_mode ? (const void*)k_basic_eval<true> : (const void*)k_basic_eval<false>);
+        const int bw = tma ? kBasicTmaWarps : kBasicEvalWarps;
+        const size_t bsmem = tma ? basic_tma_warp_bytes(B.ld) * kBasicTmaWarps : kBasicEvalSmem;
+        if (int rc = set_smem(fb, bsmem)) return rc;
         int bper = 1;
-        APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bper, fb, 32 * kBasicEvalWarps, kBasicEvalSmem));
+        APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bper, fb, 32 * bw, bsmem));
         if (bper < 1) bper = 1;
         const long long groups = ((long long)B.n_rows + 31) / 32;
-        const long long bneed = (groups + kBasicEvalWarps - 1) / kBasicEvalWarps;
+        const long long bneed = (groups + bw - 1) / bw;
         const long long bcap = (long long)bper * num_sms();
         void* bargs[] = {(void*)&B};
-        APO_CUDA(cudaLaunchKernel(fb, dim3((unsigned)(bneed < bcap ? bneed : bcap)), dim3(32 * kBasicEvalWarps), bargs,
-                                  kBasicEvalSmem, st));
+        APO_CUDA(cudaLaunchKernel(fb, dim3((unsigned)(bneed < bcap ? bneed : bcap)), dim3(32 * bw), bargs, bsmem, st));
         return APO_OK;
     }
     if (gemm) {

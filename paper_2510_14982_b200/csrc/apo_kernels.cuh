@@ -692,15 +692,152 @@ struct BasicEvalArgs {
 
 __host__ __device__ inline bool basic_split_code(int code) { return code >= OBJ_SPHERE && code <= OBJ_GRIEWANK; }
 
-constexpr int kBasicEvalWarps = 8;
-constexpr size_t kBasicEvalSmem = (size_t)kBasicEvalWarps * 32 * 33 * 8;  // one 32 x 33 block per warp
+// The reference's loop (numba_backend.py:96-131) as a running state over a candidate's elements in order.
+struct BasicFold {
+    double s = 0.0, s2 = 0.0, p = 1.0, first = 0.0, prev = 0.0;
+    __device__ __forceinline__ void add(int code, const double* table, int d, double c) {
+        switch (code) {
+        case OBJ_SPHERE: s += c * c; break;
+        case OBJ_BENT_CIGAR:
+            if (d == 0) first = c * c;
+            else s += c * c;
+            break;
+        case OBJ_ELLIPTIC: s += (table[d] * c) * c; break;
+        case OBJ_HGBAT:
+            s += c;
+            s2 += c * c;
+            break;
+        case OBJ_ROSENBROCK:
+            if (d >= 1) {
+                const double a = c - prev * prev;
+                const double b = prev - 1.0;
+                s += 100.0 * (a * a) + b * b;
+            }
+            prev = c;
+            break;
+        default:  // OBJ_GRIEWANK
+            s += c * c;
+            p *= cos_glibc(c / sqrt((double)d + 1.0));
+            break;
+        }
+    }
+    __device__ __forceinline__ double value(int code, int dim) const {
+        switch (code) {
+        case OBJ_SPHERE:
+        case OBJ_ELLIPTIC:
+        case OBJ_ROSENBROCK: return s;
+        case OBJ_BENT_CIGAR: return first + 1e6 * s;
+        case OBJ_HGBAT: return sqrt(fabs(s2 * s2 - s * s)) + (0.5 * s2 + s) / (double)dim + 0.5;
+        default: return 1.0 + s / 4000.0 - p;
+        }
+    }
+};
+
+// Greedy select of row r (numba_backend.py:270-290), rejected rows restored in dense mode.
+template <bool SEL>
+__device__ __forceinline__ void basic_select(const BasicEvalArgs& A, int g0, int nb, int lane, uint8_t cur, double nf,
+                                             unsigned long long& my_min, unsigned& my_warn) {
+    const int r = g0 + lane;
+    const bool live = lane < nb;
+    bool acc = false;
+    if (live) {
+        const double fit_i = A.fit[(!SEL && A.order) ? A.order[r] : r];
+        double kept = fit_i;
+        bool warned = false;
+        if (A.cand_ok[r] && isfinite(nf)) {
+            acc = nf < fit_i;
+            if (acc) kept = nf;
+        } else {
+            warned = true;
+        }
+        A.out_fit[r] = kept;
+        if constexpr (SEL) {
+            A.sel_next[r] = acc ? (uint8_t)(cur ^ 1) : cur;
+        } else {
+            if (A.out_acc) A.out_acc[r] = acc ? 1 : 0;
+            if (A.out_warn) A.out_warn[r] = warned ? 1 : 0;
+        }
+        const unsigned long long k = sort_key(kept);
+        my_min = k < my_min ? k : my_min;
+        my_warn += warned ? 1u : 0u;
+    }
+    if constexpr (!SEL) {
+        unsigned rej = __ballot_sync(kFull, live && !acc);
+        while (rej) {
+            const int j = __ffs(rej) - 1;
+            rej &= rej - 1;
+            const int old_row = A.order ? A.order[g0 + j] : g0 + j;
+            const double* x = A.pos + (size_t)old_row * A.ld;
+            double* dst = A.out_pos + (size_t)(g0 + j) * A.ld;
+            for (int d = lane; d < A.dim; d += 32) dst[d] = x[d];
+        }
+    }
+}
+
+// Whole rows staged by TMA (rows of 16-byte multiples, D <= kBasicTmaMaxDim): lane j bulk-copies row j
+// of its warp's 32 into shared memory (row stride ld + 2 doubles), then every lane folds its own row.
+constexpr int kBasicTmaMaxDim = 128;
+constexpr int kBasicTmaWarps = 2;
+__host__ __device__ inline int basic_tma_stride(int ld) { return ld + 2; }
+__host__ __device__ inline size_t basic_tma_warp_bytes(int ld) { return 32 * 8 * (size_t)basic_tma_stride(ld) + 16; }
+
+template <bool SEL>
+__global__ void __launch_bounds__(32 * kBasicTmaWarps) k_basic_eval_tma(BasicEvalArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int rs = basic_tma_stride(A.ld);
+    double* T = reinterpret_cast<double*>(smem + (size_t)warp * basic_tma_warp_bytes(A.ld));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(T + 32 * (size_t)rs);
+    if (lane == 0) mbar_init(bar, 1);
+    mbar_fence_init();
+    __syncwarp();
+    unsigned phase = 0;
+    const int dim = A.dim, code = A.O.code;
+    const unsigned bytes = (unsigned)(8 * A.ld);
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    const int ngroups = (A.n_rows + 31) / 32;
+    for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
+        const int g0 = A.row0 + grp * 32;
+        const int nb = min(32, A.row0 + A.n_rows - g0);
+        const int r = g0 + lane;
+        const bool live = lane < nb;
+        uint8_t cur = 0;
+        if constexpr (SEL) cur = live ? A.sel[r] : 0;
+        fence_proxy_async();  // every lane read its previous row through the generic proxy
+        if (lane == 0) mbar_expect_tx(bar, bytes * (unsigned)nb);
+        __syncwarp();
+        if (live) {
+            const double* src = SEL ? (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
+            bulk_g2s(T + (size_t)lane * rs, src, bytes, bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        BasicFold f;
+        if (live) {
+            const double* row = T + (size_t)lane * rs;
+            for (int d = 0; d < dim; d++) f.add(code, A.O.table, d, row[d]);
+        }
+        basic_select<SEL>(A, g0, nb, lane, cur, f.value(code, dim), my_min, my_warn);
+        __syncwarp();  // T is refilled by the next group's copies
+    }
+    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
+}
+
+// Any row stride: 32 x 32 blocks moved with 8-byte cp.async (coalesced), double-buffered.
+constexpr int kBasicEvalWarps = 4;
+constexpr size_t kBasicEvalWarpBytes = 2 * 32 * 33 * 8 + 32 * 8;  // two 32 x 33 blocks + 32 row pointers
+constexpr size_t kBasicEvalSmem = (size_t)kBasicEvalWarps * kBasicEvalWarpBytes;
 
 template <bool SEL>
 __global__ void __launch_bounds__(32 * kBasicEvalWarps) k_basic_eval(BasicEvalArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    double(*T)[33] = reinterpret_cast<double(*)[33]>(smem) + (size_t)warp * 32;
+    unsigned char* wbase = smem + (size_t)warp * kBasicEvalWarpBytes;
+    double(*T)[32][33] = reinterpret_cast<double(*)[32][33]>(wbase);  // [2 buffers][row][column]
+    const double** rows = reinterpret_cast<const double**>(wbase + 2 * 32 * 33 * 8);
     const int dim = A.dim, code = A.O.code;
+    const int nblk = (dim + 31) / 32;
     unsigned long long my_min = ~0ull;
     unsigned my_warn = 0;
     const int ngroups = (A.n_rows + 31) / 32;
@@ -711,96 +848,35 @@ __global__ void __launch_bounds__(32 * kBasicEvalWarps) k_basic_eval(BasicEvalAr
         const bool live = lane < nb;
         uint8_t cur = 0;
         if constexpr (SEL) cur = live ? A.sel[r] : 0;
-        // running state of the reference's loop (numba_backend.py:96-131)
-        double s = 0.0, s2 = 0.0, p = 1.0, first = 0.0, prev = 0.0;
-        for (int d0 = 0; d0 < dim; d0 += 32) {
-            const int w = min(32, dim - d0);
-            for (int j = 0; j < nb; j++) {  // row g0 + j, columns d0 .. d0 + w: one coalesced read
-                const int rj = g0 + j;
-                const double* src;
-                if constexpr (SEL) {
-                    const uint8_t sj = __shfl_sync(kFull, cur, j);
-                    src = (sj ? A.pos0 : A.pos1) + (size_t)rj * A.ld;  // the alternate buffer
-                } else {
-                    src = A.out_pos + (size_t)rj * A.ld;
-                }
-                if (lane < w) T[j][lane] = src[d0 + lane];
-            }
-            __syncwarp();
-            if (live) {
-                for (int k = 0; k < w; k++) {
-                    const int d = d0 + k;
-                    const double c = T[lane][k];
-                    switch (code) {
-                    case OBJ_SPHERE: s += c * c; break;
-                    case OBJ_BENT_CIGAR:
-                        if (d == 0) first = c * c;
-                        else s += c * c;
-                        break;
-                    case OBJ_ELLIPTIC: s += (A.O.table[d] * c) * c; break;
-                    case OBJ_HGBAT:
-                        s += c;
-                        s2 += c * c;
-                        break;
-                    case OBJ_ROSENBROCK:
-                        if (d >= 1) {
-                            const double a = c - prev * prev;
-                            const double b = prev - 1.0;
-                            s += 100.0 * (a * a) + b * b;
-                        }
-                        prev = c;
-                        break;
-                    default:  // OBJ_GRIEWANK
-                        s += c * c;
-                        p *= cos_glibc(c / sqrt((double)d + 1.0));
-                        break;
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        double nf = 0.0;
-        switch (code) {
-        case OBJ_SPHERE:
-        case OBJ_ELLIPTIC:
-        case OBJ_ROSENBROCK: nf = s; break;
-        case OBJ_BENT_CIGAR: nf = first + 1e6 * s; break;
-        case OBJ_HGBAT: nf = sqrt(fabs(s2 * s2 - s * s)) + (0.5 * s2 + s) / (double)dim + 0.5; break;
-        default: nf = 1.0 + s / 4000.0 - p; break;
-        }
-        bool acc = false;
         if (live) {
-            const double fit_i = A.fit[(!SEL && A.order) ? A.order[r] : r];
-            double kept = fit_i;
-            bool warned = false;
-            if (A.cand_ok[r] && isfinite(nf)) {
-                acc = nf < fit_i;
-                if (acc) kept = nf;
-            } else {
-                warned = true;
-            }
-            A.out_fit[r] = kept;
-            if constexpr (SEL) {
-                A.sel_next[r] = acc ? (uint8_t)(cur ^ 1) : cur;
-            } else {
-                if (A.out_acc) A.out_acc[r] = acc ? 1 : 0;
-                if (A.out_warn) A.out_warn[r] = warned ? 1 : 0;
-            }
-            const unsigned long long k = sort_key(kept);
-            my_min = k < my_min ? k : my_min;
-            my_warn += warned ? 1u : 0u;
+            if constexpr (SEL) rows[lane] = (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld;  // the alternate buffer
+            else rows[lane] = A.out_pos + (size_t)r * A.ld;
         }
-        if constexpr (!SEL) {  // rejected rows get the old row back (numba_backend.py:286-288)
-            unsigned rej = __ballot_sync(kFull, live && !acc);
-            while (rej) {
-                const int j = __ffs(rej) - 1;
-                rej &= rej - 1;
-                const int old_row = A.order ? A.order[g0 + j] : g0 + j;
-                const double* x = A.pos + (size_t)old_row * A.ld;
-                double* dst = A.out_pos + (size_t)(g0 + j) * A.ld;
-                for (int d = lane; d < dim; d += 32) dst[d] = x[d];
+        __syncwarp();
+        auto issue = [&](int b) {
+            const int d = 32 * b + lane;
+            if (d < dim)
+                for (int jr = 0; jr < nb; jr++) cp_async8(&T[b & 1][jr][lane], rows[jr] + d);
+            cp_async_commit();
+        };
+        issue(0);
+        BasicFold f;
+        for (int b = 0; b < nblk; b++) {
+            if (b + 1 < nblk) {
+                issue(b + 1);
+                cp_async_wait_prev();
+            } else {
+                cp_async_wait_all();
             }
+            __syncwarp();
+            const int d0 = 32 * b, w = min(32, dim - d0);
+            if (live) {
+                const double* trow = T[b & 1][lane];
+                for (int k = 0; k < w; k++) f.add(code, A.O.table, d0 + k, trow[k]);
+            }
+            __syncwarp();  // T[b & 1] is refilled by issue(b + 2)
         }
+        basic_select<SEL>(A, g0, nb, lane, cur, f.value(code, dim), my_min, my_warn);
     }
     block_finish(my_min, my_warn, A.warn_count, A.trace_key);
 }
