@@ -429,12 +429,11 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         B.cand_ok = cand_ok;
         B.warn_count = a.warn_count;
         B.trace_key = a.trace_key;
-        // whole rows by TMA when they are 16-byte multiples and small enough, else 32 x 32 cp.async blocks
-        const bool tma = (B.ld % 2) == 0 && dim <= kBasicTmaMaxDim;
-        const void* fb = tma ? (sel_mode ? (const void*)k_basic_eval_tma<true> : (const void*)k_basic_eval_tma<false>)
-                             : (sel_mode ? (const void*)k_basic_eval<true> : (const void*)k_basic_eval<false>);
-        const int bw = tma ? kBasicTmaWarps : kBasicEvalWarps;
-        const size_t bsmem = tma ? basic_tma_warp_bytes(B.ld) * kBasicTmaWarps : kBasicEvalSmem;
+        // 32 x 32 blocks through cp.async, double-buffered (whole rows by TMA measured slower: the fold
+        // of one group cannot overlap the copy of the next)
+        const void* fb = sel_mode ? (const void*)k_basic_eval<true> : (const void*)k_basic_eval<false>;
+        const int bw = kBasicEvalWarps;
+        const size_t bsmem = kBasicEvalSmem;
         if (int rc = set_smem(fb, bsmem)) return rc;
         int bper = 1;
         APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bper, fb, 32 * bw, bsmem));

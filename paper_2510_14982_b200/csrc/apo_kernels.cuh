@@ -774,56 +774,6 @@ __device__ __forceinline__ void basic_select(const BasicEvalArgs& A, int g0, int
     }
 }
 
-// Whole rows staged by TMA (rows of 16-byte multiples, D <= kBasicTmaMaxDim): lane j bulk-copies row j
-// of its warp's 32 into shared memory (row stride ld + 2 doubles), then every lane folds its own row.
-constexpr int kBasicTmaMaxDim = 128;
-constexpr int kBasicTmaWarps = 2;
-__host__ __device__ inline int basic_tma_stride(int ld) { return ld + 2; }
-__host__ __device__ inline size_t basic_tma_warp_bytes(int ld) { return 32 * 8 * (size_t)basic_tma_stride(ld) + 16; }
-
-template <bool SEL>
-__global__ void __launch_bounds__(32 * kBasicTmaWarps) k_basic_eval_tma(BasicEvalArgs A) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int rs = basic_tma_stride(A.ld);
-    double* T = reinterpret_cast<double*>(smem + (size_t)warp * basic_tma_warp_bytes(A.ld));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(T + 32 * (size_t)rs);
-    if (lane == 0) mbar_init(bar, 1);
-    mbar_fence_init();
-    __syncwarp();
-    unsigned phase = 0;
-    const int dim = A.dim, code = A.O.code;
-    const unsigned bytes = (unsigned)(8 * A.ld);
-    unsigned long long my_min = ~0ull;
-    unsigned my_warn = 0;
-    const int ngroups = (A.n_rows + 31) / 32;
-    for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
-        const int g0 = A.row0 + grp * 32;
-        const int nb = min(32, A.row0 + A.n_rows - g0);
-        const int r = g0 + lane;
-        const bool live = lane < nb;
-        uint8_t cur = 0;
-        if constexpr (SEL) cur = live ? A.sel[r] : 0;
-        fence_proxy_async();  // every lane read its previous row through the generic proxy
-        if (lane == 0) mbar_expect_tx(bar, bytes * (unsigned)nb);
-        __syncwarp();
-        if (live) {
-            const double* src = SEL ? (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
-            bulk_g2s(T + (size_t)lane * rs, src, bytes, bar);
-        }
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-        BasicFold f;
-        if (live) {
-            const double* row = T + (size_t)lane * rs;
-            for (int d = 0; d < dim; d++) f.add(code, A.O.table, d, row[d]);
-        }
-        basic_select<SEL>(A, g0, nb, lane, cur, f.value(code, dim), my_min, my_warn);
-        __syncwarp();  // T is refilled by the next group's copies
-    }
-    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
-}
-
 // Any row stride: 32 x 32 blocks moved with 8-byte cp.async (coalesced), double-buffered.
 constexpr int kBasicEvalWarps = 4;
 constexpr size_t kBasicEvalWarpBytes = 2 * 32 * 33 * 8 + 32 * 8;  // two 32 x 33 blocks + 32 row pointers
