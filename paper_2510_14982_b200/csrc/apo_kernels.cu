@@ -429,11 +429,15 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         B.cand_ok = cand_ok;
         B.warn_count = a.warn_count;
         B.trace_key = a.trace_key;
-        // 32 x 32 blocks through cp.async, double-buffered (whole rows by TMA measured slower: the fold
-        // of one group cannot overlap the copy of the next)
-        const void* fb = sel_mode ? (const void*)k_basic_eval<true> : (const void*)k_basic_eval<false>;
-        const int bw = kBasicEvalWarps;
-        const size_t bsmem = kBasicEvalSmem;
+        // even row strides: each lane streams its row with 16-byte loads (APO_BASIC_EVAL=1 forces the
+        // staged form); odd strides: 32 x 32 blocks through cp.async, double-buffered.  (Whole rows by
+        // TMA measured slower: the fold of one group cannot overlap the copy of the next.)
+        static const int env_be = getenv("APO_BASIC_EVAL") ? atoi(getenv("APO_BASIC_EVAL")) : 0;
+        const bool direct = (B.ld % 2) == 0 && env_be != 1;
+        const void* fb = direct ? (sel_mode ? (const void*)k_basic_eval_direct<true> : (const void*)k_basic_eval_direct<false>)
+                                : (sel_mode ? (const void*)k_basic_eval<true> : (const void*)k_basic_eval<false>);
+        const int bw = direct ? kBasicDirectWarps : kBasicEvalWarps;
+        const size_t bsmem = direct ? 0 : kBasicEvalSmem;
         if (int rc = set_smem(fb, bsmem)) return rc;
         int bper = 1;
         APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bper, fb, 32 * bw, bsmem));

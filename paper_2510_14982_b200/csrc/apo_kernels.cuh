@@ -774,6 +774,42 @@ __device__ __forceinline__ void basic_select(const BasicEvalArgs& A, int g0, int
     }
 }
 
+// Even row strides: no staging at all -- each lane streams its own candidate row with 16-byte loads
+// (a warp instruction touches 32 rows, the second half of each 32-byte sector follows from L1) and folds
+// it in registers; small enough to run 48 warps per SM, so the row streams of many warps overlap.
+constexpr int kBasicDirectWarps = 8;
+template <bool SEL>
+__global__ void __launch_bounds__(32 * kBasicDirectWarps) k_basic_eval_direct(BasicEvalArgs A) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int dim = A.dim, code = A.O.code;
+    unsigned long long my_min = ~0ull;
+    unsigned my_warn = 0;
+    const int ngroups = (A.n_rows + 31) / 32;
+    for (int grp = blockIdx.x * nwarps + warp; grp < ngroups; grp += gridDim.x * nwarps) {
+        const int g0 = A.row0 + grp * 32;
+        const int nb = min(32, A.row0 + A.n_rows - g0);
+        const int r = g0 + lane;
+        const bool live = lane < nb;
+        uint8_t cur = 0;
+        if constexpr (SEL) cur = live ? A.sel[r] : 0;
+        BasicFold f;
+        if (live) {
+            const double* row = SEL ? (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
+            const double2* row2 = reinterpret_cast<const double2*>(row);
+            const int h = dim >> 1;
+#pragma unroll 4
+            for (int k = 0; k < h; k++) {
+                const double2 v = __ldcs(row2 + k);  // streamed once: evict-first
+                f.add(code, A.O.table, 2 * k, v.x);
+                f.add(code, A.O.table, 2 * k + 1, v.y);
+            }
+            if (dim & 1) f.add(code, A.O.table, dim - 1, __ldcs(row + dim - 1));
+        }
+        basic_select<SEL>(A, g0, nb, lane, cur, f.value(code, dim), my_min, my_warn);
+    }
+    block_finish(my_min, my_warn, A.warn_count, A.trace_key);
+}
+
 // Any row stride: 32 x 32 blocks moved with 8-byte cp.async (coalesced), double-buffered.
 constexpr int kBasicEvalWarps = 4;
 constexpr size_t kBasicEvalWarpBytes = 2 * 32 * 33 * 8 + 32 * 8;  // two 32 x 33 blocks + 32 row pointers
