@@ -404,6 +404,12 @@ def bench_ours(args, rank, world, local):
         result["suite_c5"] = bench_c5()
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(m["cfg"], args.objective)
+        try:
+            ros = result.get("c4_rosenbrock", {})
+            result["cpu_baseline_numba"] = cpu_baseline_numba(
+                {"value": ros.get("value"), "line": "c4_rosenbrock"} if ros else None)
+        except Exception as exc:  # a reported baseline: never lose the main line over it
+            result["cpu_baseline_numba"] = {"unavailable": f"{type(exc).__name__}: {exc}"[:200]}
     return result
 
 
@@ -699,6 +705,43 @@ def cpu_baseline(cfg, objective, max_seconds=25.0):
             "sample": f"{done} full iterations of ps={cfg.ps} D={cfg.dim} {objective} "
                       "(oracle.step: stable sort + gather + coordinator + OpenMP update)",
             "cpu": _cpu_model()}
+
+
+def cpu_baseline_numba(gpu_line=None, ps=1_000_000, dim=100, steps=3, max_seconds=60.0):
+    """BASELINE.md §2's CPU baseline: the UNMODIFIED reference (baseline/_ref, numba backend, parallel
+    mode on every host core) stepping the C4 shape on its own objective rosenbrock, JIT warm-up excluded
+    (as compare_backends.py:56).  The initial population is the oracle's (bit-identical to the reference's
+    initialize, which alone takes ~30 s of Python at this size)."""
+    ref_site = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_site, "protozoa")):
+        return {"unavailable": "reference not installed in baseline/_ref"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "numba_cache_bench"))
+    sys.path.insert(0, ref_site)
+    try:
+        import protozoa
+    finally:
+        sys.path.remove(ref_site)
+    import oracle
+
+    nthreads = os.cpu_count() or 1
+    cfg = protozoa.ApoConfig(ps=ps, dim=dim, bounds=protozoa.Bounds(-100.0, 100.0, dim), max_iterations=25, seed=0)
+    mode = protozoa.EngineMode.parallel(nthreads)
+    small = protozoa.ApoConfig(ps=64, dim=dim, bounds=protozoa.Bounds(-100.0, 100.0, dim), max_iterations=3)
+    protozoa.step(protozoa.initialize(small, "rosenbrock"), small, "rosenbrock", 0, mode)  # numba JIT
+    pos, fit = oracle.initialize(0, ps, dim, -100.0, 100.0, "rosenbrock")
+    pop = protozoa.Population(pos, fit, iteration=0, fe_count=ps)
+    done, t0 = 0, time.perf_counter()
+    while done < steps and time.perf_counter() - t0 < max_seconds:
+        pop = protozoa.step(pop, cfg, "rosenbrock", done, mode)
+        done += 1
+    dt = time.perf_counter() - t0
+    out = {"value": ps * done / dt, "unit": UNIT, "cores": nthreads, "kind": "reference",
+           "sample": f"{done} protozoa.step iterations (numba backend, EngineMode.parallel({nthreads})) of "
+                     f"ps={ps} D={dim} rosenbrock, JIT excluded",
+           "cpu": _cpu_model()}
+    if gpu_line:
+        out["gpu_same_workload"] = gpu_line
+    return out
 
 
 def _cpu_model():
