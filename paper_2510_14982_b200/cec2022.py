@@ -64,9 +64,15 @@ class CecFunction:
 
     fn: int
     data_seed: int = 2022
-    # "dmma": tensor-core rotation (k_cec_eval / quad evaluator, dim <= 104);
-    # "fma": lane-per-output FMA rotation through L1 (BASELINE config 5's comparison path)
-    rotation: str = "dmma"
+    # "dmma": tensor-core rotation (k_cec_eval / quad evaluator, dim <= 104; the N x D x D GEMM above);
+    # "fma": lane-per-output FMA rotation through L1 (BASELINE config 5's comparison path);
+    # "auto": FMA up to FMA_MAX_DIM, where the rotation is too small to pay for the split launch, DMMA above
+    rotation: str = "auto"
+
+    def rotation_for(self, dim: int) -> str:
+        if self.rotation == "auto":
+            return "fma" if dim <= FMA_MAX_DIM else "dmma"
+        return self.rotation
 
     def arrays(self, dim: int):
         return cec_data(self.fn, dim, self.data_seed)
@@ -79,15 +85,19 @@ class CecFunction:
         return FSTAR[self.fn - 1]
 
 
+# measured crossover of the DMMA and FMA rotations (profiles/r01_c5_sweep.txt, r02 C5 sweep): at D <= 20
+# the fused FMA update is one launch and wins; from D = 50 the DMMA evaluation kernel does
+FMA_MAX_DIM = 20
+
 # hybrids split D into ceil(p_k D)-sized segments; F7/F8 need D >= 5 for that to fit
 MIN_DIM = (2, 2, 2, 2, 2, 2, 5, 5, 2, 2, 2, 2)
 
 
-def cec2022_objective(fn: int, data_seed: int = 2022, rotation: str = "dmma") -> Objective:
+def cec2022_objective(fn: int, data_seed: int = 2022, rotation: str = "auto") -> Objective:
     if not (isinstance(fn, int) and 1 <= fn <= 12):
         raise ValueError(f"CEC2022 function index must be 1..12, got {fn!r}")
-    if rotation not in ("dmma", "fma"):
-        raise ValueError(f"rotation must be 'dmma' or 'fma', got {rotation!r}")
+    if rotation not in ("auto", "dmma", "fma"):
+        raise ValueError(f"rotation must be 'auto', 'dmma' or 'fma', got {rotation!r}")
     return _cec2022_objective(fn, data_seed, rotation)
 
 
@@ -95,14 +105,17 @@ def cec2022_objective(fn: int, data_seed: int = 2022, rotation: str = "dmma") ->
 def _cec2022_objective(fn: int, data_seed: int, rotation: str) -> Objective:
     # one instance per (fn, data, rotation): its device tables (objectives.device_objective) are built
     # once, not once per run of a batch
-    name = f"cec2022_f{fn}" + ("" if rotation == "dmma" else "_fma")
+    name = f"cec2022_f{fn}" + ("" if rotation == "auto" else "_" + rotation)
     return Objective(name, CEC2022_BASE + fn, min_dim=MIN_DIM[fn - 1], data=CecFunction(fn, data_seed, rotation))
 
 
 def _resolve(name: str):
     key = name.strip().lower()
-    if key.startswith("cec2022_f") and key.endswith("_fma") and key[9:-4].isdigit() and 1 <= int(key[9:-4]) <= 12:
-        return cec2022_objective(int(key[9:-4]), rotation="fma")
+    for rot in ("fma", "dmma"):  # explicit rotation: cec2022_f6_fma, cec2022_f6_dmma
+        tail = "_" + rot
+        if key.startswith("cec2022_f") and key.endswith(tail) and key[9:-len(tail)].isdigit() \
+                and 1 <= int(key[9:-len(tail)]) <= 12:
+            return cec2022_objective(int(key[9:-len(tail)]), rotation=rot)
     for prefix in ("cec2022_f", "cec2022-f", "f"):
         if key.startswith(prefix) and key[len(prefix):].isdigit():
             k = int(key[len(prefix):])

@@ -174,7 +174,8 @@ class DeviceObjective:
             shift, rot, shuffle = obj.data.arrays(dim)
             rot_t = np.ascontiguousarray(np.transpose(rot, (0, 2, 1)))
             arrays = [("shift", shift), ("rot_t", rot_t), ("shuffle", shuffle)]
-            if dim <= 104 and getattr(obj.data, "rotation", "dmma") == "dmma":
+            rotation = data.rotation_for(dim) if hasattr(data, "rotation_for") else getattr(data, "rotation", "dmma")
+            if dim <= 104 and rotation == "dmma":
                 # zero-padded M^T for the DMMA evaluation kernel (include/apo_b200.h)
                 nt = 2 if dim <= 16 else 4 if dim <= 32 else 7 if dim <= 56 else 13
                 n4 = (dim + 3) // 4 * 4
@@ -184,7 +185,7 @@ class DeviceObjective:
                     pad[0, :dim, :dim] = rot_t[0][:, np.asarray(shuffle) - 1]
                 arrays.append(("rot_pad", pad))
                 table = elliptic_weights(dim)  # ELLIPS weights 10^(6i/(D-1)), host libm like the oracle
-            elif getattr(obj.data, "rotation", "dmma") == "dmma" and obj.code - 100 in (1, 2, 3, 4, 5, 6, 7, 8, 10):
+            elif rotation == "dmma" and obj.code - 100 in (1, 2, 3, 4, 5, 6, 7, 8, 10):
                 # D > 104: the rotated component's M^T padded for the DMMA GEMM (apo_cec_gemm.cu)
                 comp = 1 if obj.code - 100 == 10 else 0
                 kp, np_ = (dim + 15) // 16 * 16, (dim + 63) // 64 * 64

@@ -26,7 +26,8 @@ def raw_metrics(path):
         i = h.index(name)
         v = float(vals[i].replace(",", ""))
         u = units[i]
-        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+                    "msecond": 1e6, "second": 1e9}.get(u, 1)
 
     d = {"dram_bytes": get("dram__bytes_read.sum") + get("dram__bytes_write.sum"),
          "duration_ns": get("gpu__time_duration.sum")}
