@@ -651,7 +651,7 @@ def bench_c5(sizes=(10, 20, 50, 100, 1000), fns=(1, 4, 10), ps=10_000, iters=20,
     rows = []
     for fn in fns:
         for dim in sizes:
-            for rot in ("dmma", "fma"):
+            for rot in ("dmma", "fma", "auto"):  # auto: what the library picks (FMA on this path at D <= 32)
                 obj = pz.cec2022_objective(fn, rotation=rot)
                 cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-100.0, 100.0, dim), max_iterations=iters + 3)
                 run = DeviceRun(cfg, obj)

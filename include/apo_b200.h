@@ -83,7 +83,12 @@ typedef struct apo_objective {
      * permuted like rot_pad).  When present, the device loop rotates all
      * candidates of an iteration as one DMMA GEMM (apo_cec_gemm.cu). */
     const double *rot_gemm;
+    /* APO_OBJ_FMA_SMALL_D: with rot_pad present, the device loop may still rotate with lane-per-output
+     * FMAs (the one-kernel fused update) at dim <= 32, where that is faster; batches keep the DMMA
+     * evaluator at every dim (measured: profiles/r02_c5_rotation_crossover.txt). */
+    int32_t flags;
 } apo_objective;
+#define APO_OBJ_FMA_SMALL_D 1
 
 int apo_abi_version(void);
 const char *apo_last_error(void);

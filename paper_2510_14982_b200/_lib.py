@@ -111,7 +111,7 @@ _INT = C.c_int
 class apo_objective(C.Structure):
     _fields_ = [("code", C.c_int32), ("table_len", C.c_int32), ("table", C.c_void_p), ("shift", C.c_void_p),
                 ("rot_t", C.c_void_p), ("shuffle", C.c_void_p), ("rot_pad", C.c_void_p),
-                ("rot_gemm", C.c_void_p)]
+                ("rot_gemm", C.c_void_p), ("flags", C.c_int32)]
 
 
 PROTOTYPES = {

@@ -66,13 +66,9 @@ class CecFunction:
     data_seed: int = 2022
     # "dmma": tensor-core rotation (k_cec_eval / quad evaluator, dim <= 104; the N x D x D GEMM above);
     # "fma": lane-per-output FMA rotation through L1 (BASELINE config 5's comparison path);
-    # "auto": FMA up to FMA_MAX_DIM, where the rotation is too small to pay for the split launch, DMMA above
+    # "auto": DMMA, except the device-resident loop at D <= 32, where the one-kernel FMA update wins
+    # (APO_OBJ_FMA_SMALL_D; shared-memory batches keep DMMA at every D, where it is ~1.8x faster)
     rotation: str = "auto"
-
-    def rotation_for(self, dim: int) -> str:
-        if self.rotation == "auto":
-            return "fma" if dim <= FMA_MAX_DIM else "dmma"
-        return self.rotation
 
     def arrays(self, dim: int):
         return cec_data(self.fn, dim, self.data_seed)
@@ -84,10 +80,6 @@ class CecFunction:
     def fstar(self) -> float:
         return FSTAR[self.fn - 1]
 
-
-# measured crossover of the DMMA and FMA rotations (profiles/r01_c5_sweep.txt, r02 C5 sweep): at D <= 20
-# the fused FMA update is one launch and wins; from D = 50 the DMMA evaluation kernel does
-FMA_MAX_DIM = 20
 
 # hybrids split D into ceil(p_k D)-sized segments; F7/F8 need D >= 5 for that to fit
 MIN_DIM = (2, 2, 2, 2, 2, 2, 5, 5, 2, 2, 2, 2)

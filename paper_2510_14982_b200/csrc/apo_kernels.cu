@@ -109,6 +109,7 @@ ObjDesc to_desc(const apo_objective* o) {
     d.cec.shuffle = o->shuffle;
     d.cec.rot_pad = o->rot_pad;
     d.cec.rot_gemm = o->rot_gemm;
+    d.flags = o->flags;
     return d;
 }
 
@@ -251,30 +252,35 @@ __global__ void k_gather_rows(int n, int dim, int ld, const double* __restrict__
     }
 }
 
+// kHistCopies sub-histograms per warp (lane % kHistCopies picks one; stride 257 words so the copies of a
+// bin sit in different banks): real images concentrate on a few hot bins, and lanes of one warp hitting
+// the same shared-memory word serialise.
+constexpr int kHistCopies = 4;
 __global__ void k_histogram_u8(const uint8_t* __restrict__ px, long long n, unsigned long long* __restrict__ counts) {
-    __shared__ unsigned h[kWarps][256];
-    const int warp = threadIdx.x >> 5;
-    for (int k = threadIdx.x; k < kWarps * 256; k += blockDim.x) (&h[0][0])[k] = 0u;
+    __shared__ unsigned h[kWarps * kHistCopies * 257];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned* mine = h + (warp * kHistCopies + (lane % kHistCopies)) * 257;
+    for (int k = threadIdx.x; k < kWarps * kHistCopies * 257; k += blockDim.x) h[k] = 0u;
     __syncthreads();
     const long long nvec = n / 16;
     const uint4* v = reinterpret_cast<const uint4*>(px);
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nvec;
          q += (long long)gridDim.x * blockDim.x) {
-        const uint4 w = v[q];
+        const uint4 w = __ldcs(v + q);  // streamed once
         const unsigned words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int a = 0; a < 4; a++) {
 #pragma unroll
-            for (int b = 0; b < 4; b++) atomicAdd(&h[warp][(words[a] >> (8 * b)) & 0xFFu], 1u);
+            for (int b = 0; b < 4; b++) atomicAdd(&mine[(words[a] >> (8 * b)) & 0xFFu], 1u);
         }
     }
     for (long long q = nvec * 16 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
          q += (long long)gridDim.x * blockDim.x)
-        atomicAdd(&h[warp][px[q]], 1u);
+        atomicAdd(&mine[px[q]], 1u);
     __syncthreads();
     for (int b = threadIdx.x; b < 256; b += blockDim.x) {
         unsigned long long s = 0;
-        for (int w = 0; w < kWarps; w++) s += h[w][b];
+        for (int w = 0; w < kWarps * kHistCopies; w++) s += h[w * 257 + b];
         if (s) atomicAdd(&counts[b], s);
     }
 }
@@ -334,8 +340,10 @@ int launch_cec_eval(bool sel_mode, const UpdArgs& a, cudaStream_t st, uint8_t* c
 // or CEC2022 without DMMA tables), 1 CEC2022 split (k_update_group candidates + k_cec_eval), 2 fused
 // CEC2022 (k_update_cec), 3 CEC2022 GEMM (candidates + k_dgemm_nn + k_cec_finish), 4 the reference's
 // objectives split (candidates + k_basic_eval).
-int update_path(bool sel_mode, const UpdArgs& a, bool have_cand_ok, bool have_counter) {
+int update_path(bool sel_mode, const UpdArgs& a0, bool have_cand_ok, bool have_counter) {
+    UpdArgs a = a0;
     const int dim = a.P.dim;
+    if ((a.O.flags & APO_OBJ_FMA_SMALL_D) && dim <= 32) a.O.cec.rot_pad = nullptr;  // launch_update does the same
     const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
     const bool cec = have_cand_ok && a.O.code > APO_OBJ_CEC2022_BASE;
     if (cec && dim <= kGroupMaxDim && dim <= kCecEvalMaxDim && a.O.cec.rot_pad != nullptr) {
@@ -352,10 +360,13 @@ int update_path(bool sel_mode, const UpdArgs& a, bool have_cand_ok, bool have_co
     return 0;
 }
 
+constexpr int kCecFmaMaxDim = 32;  // the fused FMA rotation beats the DMMA split up to here (device loop)
+
 int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* cand_ok = nullptr,
                   cudaEvent_t mid_event = nullptr, unsigned* tile_counter = nullptr) {
     UpdArgs a = A0;
     const int dim = a.P.dim;
+    if ((a.O.flags & APO_OBJ_FMA_SMALL_D) && dim <= kCecFmaMaxDim) a.O.cec.rot_pad = nullptr;  // FMA rotation
     const bool group = dim <= kGroupMaxDim;
     const int fn_id = a.O.code - APO_OBJ_CEC2022_BASE;
     const bool split = group && cand_ok && a.O.code > APO_OBJ_CEC2022_BASE && dim <= kCecEvalMaxDim &&
@@ -657,7 +668,7 @@ struct apo_run {
 
 extern "C" {
 
-int apo_abi_version(void) { return 2; }  // 2: rng arguments, shard/load/threshold entry points
+int apo_abi_version(void) { return 3; }  // 3: apo_objective.flags, apo_run_updates_ordered; 2: rng, shard/load/threshold
 
 const char* apo_last_error(void) { return g_err.c_str(); }
 
@@ -772,7 +783,7 @@ int apo_run_updates(const double* positions, const double* fitness, const uint8_
                     double p_ah, double f_mult, double decay, int64_t code, const double* table, int64_t table_len,
                     const double* p_dr, unsigned long long* warn_count, void* stream) {
     APO_CHECK(span == upper - lower, "span must equal upper - lower");
-    apo_objective o;
+    apo_objective o{};
     o.code = (int32_t)code;
     o.table_len = (int32_t)table_len;
     o.table = table;

@@ -32,6 +32,7 @@ struct ObjDesc {
     int table_len;
     const double* table;  // elliptic weights (code 2) or value table (code 6)
     CecData cec;          // CEC2022 data (code OBJ_CEC_BASE + F)
+    int flags;            // APO_OBJ_FMA_SMALL_D (include/apo_b200.h)
 };
 
 __device__ __forceinline__ double warp_bcast(double v, int src) { return __shfl_sync(0xFFFFFFFFu, v, src); }

@@ -174,7 +174,10 @@ class DeviceObjective:
             shift, rot, shuffle = obj.data.arrays(dim)
             rot_t = np.ascontiguousarray(np.transpose(rot, (0, 2, 1)))
             arrays = [("shift", shift), ("rot_t", rot_t), ("shuffle", shuffle)]
-            rotation = data.rotation_for(dim) if hasattr(data, "rotation_for") else getattr(data, "rotation", "dmma")
+            rotation = getattr(data, "rotation", "dmma")
+            if rotation == "auto":  # DMMA tables; the device loop may still pick FMAs at small D
+                self.struct.flags = 1  # APO_OBJ_FMA_SMALL_D
+                rotation = "dmma"
             if dim <= 104 and rotation == "dmma":
                 # zero-padded M^T for the DMMA evaluation kernel (include/apo_b200.h)
                 nt = 2 if dim <= 16 else 4 if dim <= 32 else 7 if dim <= 56 else 13
