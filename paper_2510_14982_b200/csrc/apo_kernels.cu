@@ -252,35 +252,30 @@ __global__ void k_gather_rows(int n, int dim, int ld, const double* __restrict__
     }
 }
 
-// kHistCopies sub-histograms per warp (lane % kHistCopies picks one; stride 257 words so the copies of a
-// bin sit in different banks): real images concentrate on a few hot bins, and lanes of one warp hitting
-// the same shared-memory word serialise.
-constexpr int kHistCopies = 4;
 __global__ void k_histogram_u8(const uint8_t* __restrict__ px, long long n, unsigned long long* __restrict__ counts) {
-    __shared__ unsigned h[kWarps * kHistCopies * 257];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned* mine = h + (warp * kHistCopies + (lane % kHistCopies)) * 257;
-    for (int k = threadIdx.x; k < kWarps * kHistCopies * 257; k += blockDim.x) h[k] = 0u;
+    __shared__ unsigned h[kWarps][256];
+    const int warp = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < kWarps * 256; k += blockDim.x) (&h[0][0])[k] = 0u;
     __syncthreads();
     const long long nvec = n / 16;
     const uint4* v = reinterpret_cast<const uint4*>(px);
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nvec;
          q += (long long)gridDim.x * blockDim.x) {
-        const uint4 w = __ldcs(v + q);  // streamed once
+        const uint4 w = v[q];
         const unsigned words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int a = 0; a < 4; a++) {
 #pragma unroll
-            for (int b = 0; b < 4; b++) atomicAdd(&mine[(words[a] >> (8 * b)) & 0xFFu], 1u);
+            for (int b = 0; b < 4; b++) atomicAdd(&h[warp][(words[a] >> (8 * b)) & 0xFFu], 1u);
         }
     }
     for (long long q = nvec * 16 + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
          q += (long long)gridDim.x * blockDim.x)
-        atomicAdd(&mine[px[q]], 1u);
+        atomicAdd(&h[warp][px[q]], 1u);
     __syncthreads();
     for (int b = threadIdx.x; b < 256; b += blockDim.x) {
         unsigned long long s = 0;
-        for (int w = 0; w < kWarps * kHistCopies; w++) s += h[w * 257 + b];
+        for (int w = 0; w < kWarps; w++) s += h[w][b];
         if (s) atomicAdd(&counts[b], s);
     }
 }
@@ -664,6 +659,11 @@ struct apo_run {
     // optional CUDA-event timing of the fused update launch (bench.py roofline)
     bool profile;
     std::vector<cudaEvent_t> prof_events;
+    // the coordinator's Dr draws (their own sort) run on a side stream beside the fitness sort
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    void* dr_tmp = nullptr;
+    size_t dr_tmp_bytes = 0;
 };
 
 extern "C" {
@@ -1005,11 +1005,16 @@ int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iteration
     alloc((void**)&r->dr_sorted, 8 * (size_t)r->dr_cap);
     alloc((void**)&r->dr_bits, 4 * (size_t)((ps + 31) / 32));
     alloc(&r->tmp, r->tmp_bytes);
+    r->dr_tmp_bytes = tb_dr;
+    alloc(&r->dr_tmp, r->dr_tmp_bytes);
     alloc((void**)&r->p_dr, 8 * (size_t)ps);
     alloc((void**)&r->cand_ok, (size_t)ps);
     alloc((void**)&r->tile_counter, 16);
     alloc((void**)&r->trace_keys, 8 * (size_t)(max_iterations + 1));
     alloc((void**)&r->warn, 8);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_join, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         apo_run_destroy(r);
         return fail(APO_ENOMEM, std::string("apo_run_create: ") + cudaGetErrorString(e));
@@ -1080,16 +1085,21 @@ int apo_run_iterate(apo_run* r, int64_t n) {
                                            r->keys_in, (int*)r->keys_out, num_sms(), st));
             std::swap(r->order, r->vals_in);
         } else {
-            // 1. stable sort by fitness, ties by previous rank
+            // 2. coordinator draws, forked onto the side stream (they depend only on the keys and on the
+            //    previous update having consumed dr_bits, which the fork event orders)
+            APO_CUDA(cudaEventRecord(r->ev_fork, st));
+            APO_CUDA(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
+            if (int rc = dr_device(r->rng, r->seed, key_it, r->ps, count, r->dr_keys, r->dr_sorted, r->dr_tmp,
+                                   r->dr_tmp_bytes, r->dr_bits, nullptr, r->side))
+                return rc;
+            APO_CUDA(cudaEventRecord(r->ev_join, r->side));
+            // 1. stable sort by fitness, ties by previous rank (concurrently with 2.)
             k_make_keys<<<grid_for(ps, 256), 256, 0, st>>>(ps, r->fit[r->cur], r->order, r->keys_in, r->vals_in);
             APO_CUDA(cudaGetLastError());
             size_t tb = r->tmp_bytes;
             APO_CUDA(cub::DeviceRadixSort::SortPairs(r->tmp, tb, r->keys_in, r->keys_out, r->vals_in, r->order, ps, 0,
                                                      64, st));
-            // 2. coordinator draws
-            if (int rc = dr_device(r->rng, r->seed, key_it, r->ps, count, r->dr_keys, r->dr_sorted, r->tmp,
-                                   r->tmp_bytes, r->dr_bits, nullptr, st))
-                return rc;
+            APO_CUDA(cudaStreamWaitEvent(st, r->ev_join, 0));
         }
         // 3. fused update
         IterParams P;
@@ -1282,11 +1292,15 @@ int apo_run_profile_read(apo_run* r, double* update_ms_host, int64_t* launches_h
 int apo_run_destroy(apo_run* r) {
     if (!r) return APO_OK;
     clear_profile(r);
+    if (r->side) cudaStreamSynchronize(r->side);  // nothing may still run on the side stream
     void* bufs[] = {r->pos[0], r->pos[1], r->sel[0], r->sel[1], r->fit[0], r->fit[1], r->order, r->keys_in, r->keys_out, r->vals_in,
                     r->dr_keys, r->dr_sorted, r->dr_bits, r->tmp, r->p_dr, r->trace_keys, r->warn, r->cand_ok,
-                    r->tile_counter};
+                    r->tile_counter, r->dr_tmp};
     for (void* b : bufs)
         if (b) cudaFreeAsync(b, r->stream);
+    if (r->ev_fork) cudaEventDestroy(r->ev_fork);
+    if (r->ev_join) cudaEventDestroy(r->ev_join);
+    if (r->side) cudaStreamDestroy(r->side);
     delete r;
     return APO_OK;
 }

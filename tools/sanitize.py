@@ -30,6 +30,24 @@ for ps in (3000, 30000):                   # tile sort + merge prologue, CUB pro
 ccfg = pz.ApoConfig(ps=70_000, dim=5, bounds=pz.Bounds(-5.0, 5.0, 5), max_iterations=3, seed=1)
 for name in ("rosenbrock", "cec2022_f4"):                   # step(): rank-chunked update + overlapped D2H
     pz.step(pz.initialize(ccfg, name), ccfg, name, 0)
+# round 2: the lean step (fitness first, rows read through the sort's order, basic-objective split in
+# dense mode), the one-kernel fused CEC2022 update (opt-in) and the verification entries
+lcfg = pz.ApoConfig(ps=70_000, dim=40, bounds=pz.Bounds(-5.0, 5.0, 40), max_iterations=3, seed=3)
+for name in ("rosenbrock", "griewank", "cec2022_f6"):
+    pz.step(pz.initialize(lcfg, name), lcfg, name, 1)
+os.environ["APO_CEC_FUSED"] = "1"
+engine.BATCH_PS_LIMIT = 0
+pz.run(pz.ApoConfig(ps=3000, dim=100, bounds=pz.Bounds(-100.0, 100.0, 100), max_iterations=3, seed=4), "cec2022_f10")
+del os.environ["APO_CEC_FUSED"]
+from paper_2510_14982_b200 import _lib  # noqa: E402
+
+xs = torch.linspace(-700.0, 700.0, 4096, dtype=torch.float64, device="cuda")
+ys = torch.empty_like(xs)
+_lib.check(_lib.load().apo_debug_cos(_lib.ptr(xs), _lib.ptr(ys), xs.numel(), _lib.stream_handle()))
+z = torch.rand(37, 100, dtype=torch.float64, device="cuda")
+fz = torch.empty(37, dtype=torch.float64, device="cuda")
+for variant in (0, 1):
+    _lib.check(_lib.load().apo_debug_cec_basic(9, _lib.ptr(z), 37, 100, None, _lib.ptr(fz), variant, _lib.stream_handle()))
 scfg = pz.ApoConfig(ps=16, dim=10, bounds=pz.Bounds(-5.0, 5.0, 10), max_iterations=3)
 pz.run_batch(scfg, ["cec2022_f12", "sphere", "cec2022_f7"] * 60, list(range(180)))  # persistent claims
 pz.run_batch(scfg, ["cec2022_f1"] * 4, list(range(4)), threads_per_run=64)        # explicit CTA size
