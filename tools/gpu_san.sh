@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize.py > gpurun_out/r02_$tool.log 2>&1
+  echo "$tool rc=$?"; tail -3 gpurun_out/r02_$tool.log
+done
