@@ -297,29 +297,15 @@ __device__ inline void group_phase_a(const IterParams& P, const Rows& R, int i, 
     for (int w = 0; w < g.words; w++) bits[w] = 0u;
     if (op != OP_DORMANCY && count > 0) {
         unsigned char* perm = g.perm + (size_t)lane * g.dp;
-        // identity permutation, four entries per 32-bit store (dp is a multiple of 4)
-        unsigned* perm4 = reinterpret_cast<unsigned*>(perm);
-        for (int d4 = 0; d4 < (dim + 3) >> 2; d4++) perm4[d4] = 0x03020100u + 0x04040404u * (unsigned)d4;
-        auto swap_step = [&](int j, double u) {
-            int r = j + (int)(u * (double)(dim - j));
+        for (int d = 0; d < dim; d++) perm[d] = (unsigned char)d;
+        for (int j = 0; j < count; j++) {
+            int r = j + (int)(uniform(base, kMaskBase + (uint64_t)j) * (double)(dim - j));
             if (r > dim - 1) r = dim - 1;
             const unsigned char a = perm[j], b = perm[r];
             perm[j] = b;
             perm[r] = a;
             bits[b >> 5] |= 1u << (b & 31);
-        };
-        // the draws are counter-based (independent of the chain): four in flight at a time, then the
-        // four dependent swaps in order -- the same chain, with the hash latency overlapped
-        int j = 0;
-        for (; j + 4 <= count; j += 4) {
-            const double u0 = uniform(base, kMaskBase + (uint64_t)j), u1 = uniform(base, kMaskBase + (uint64_t)j + 1);
-            const double u2 = uniform(base, kMaskBase + (uint64_t)j + 2), u3 = uniform(base, kMaskBase + (uint64_t)j + 3);
-            swap_step(j, u0);
-            swap_step(j + 1, u1);
-            swap_step(j + 2, u2);
-            swap_step(j + 3, u3);
         }
-        for (; j < count; j++) swap_step(j, uniform(base, kMaskBase + (uint64_t)j));
     }
 }
 
