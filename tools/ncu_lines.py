@@ -3,7 +3,7 @@ import csv
 import sys
 
 
-def main(path, top=30):
+def main(path, top=30, by="stall"):
     cur = None
     hdr = None
     lines = []
@@ -26,11 +26,14 @@ def main(path, top=30):
                 continue
             total += s
             lines.append((s, n, cur, int(row[0]), row[1].strip()[:90]))
-    lines.sort(reverse=True)
-    print(f"total stall samples {total:.0f}")
+    if by == "inst":
+        lines.sort(key=lambda x: -x[1])
+    else:
+        lines.sort(reverse=True)
+    print(f"total stall samples {total:.0f}  total instructions {sum(x[1] for x in lines) / 1e6:.1f}M  (sorted by {by})")
     for s, n, f, ln, src in lines[:top]:
         print(f"{100 * s / total:5.1f}% {n / 1e6:8.2f}M  {f}:{ln:<5d} {src}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30, sys.argv[3] if len(sys.argv) > 3 else "stall")
