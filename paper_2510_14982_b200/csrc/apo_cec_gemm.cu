@@ -263,8 +263,8 @@ int cec_gemm_finish(const CecGemmArgs& A0, cudaStream_t st, int num_sms) {
     dim3 grid(A.np / GBN, (A.n_rows + GBM - 1) / GBM);
     k_dgemm_nn<<<grid, 128, 0, st>>>(A.Y, A.O.cec.rot_gemm, A.Z, A.n_rows, A.kp, A.np);
     const size_t fsmem = 8 * 2 * (size_t)A.np * 8;
-    if (fsmem > 48 * 1024) cudaFuncSetAttribute((const void*)k_cec_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)fsmem);
+    // always set: the 48 KB default also has to hold the kernel's static shared memory
+    cudaFuncSetAttribute((const void*)k_cec_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
     k_cec_finish<<<pw < 8 * num_sms ? pw : 8 * num_sms, 256, fsmem, st>>>(A);
     cudaFreeAsync(A.Y, st);
     cudaFreeAsync(A.Z, st);

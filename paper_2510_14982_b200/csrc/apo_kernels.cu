@@ -38,6 +38,7 @@ thread_local std::string g_err;
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
+    if (code == APO_ECUDA) (void)cudaGetLastError();  // a failed launch must not fail the next call's check
     return code;
 }
 
@@ -94,7 +95,9 @@ int warps_for_dim(int64_t dim) {
 }
 
 int set_smem(const void* fn, size_t bytes) {
-    if (bytes > 48 * 1024) APO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    // always: the 48 KB default covers static + dynamic shared memory, so a request just under 48 KB
+    // still fails to launch once the kernel's own static arrays are added (k_run_batch, ps = 48, D = 6)
+    if (bytes > 0) APO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     return APO_OK;
 }
 

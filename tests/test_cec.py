@@ -110,9 +110,11 @@ def test_suite_batch_matches_oracle_runs():
     res = pz.run_batch(cfg, names, seeds)
     want, _ = oracle.run_many(names, seeds, ps=60, dim=20, max_iterations=40, lower=-100.0, upper=100.0)
     # free-running: a last-ulp difference at an exact fitness tie can send one run down a
-    # different (equally valid) trajectory, so most runs must agree tightly and all loosely
+    # different (equally valid) trajectory, so 90% of the runs must agree tightly and all loosely; the
+    # teacher-forced suites (test_headline_parity.py) pin every individual step at 1e-9
     rel = np.abs(res.best_fitness - want) / np.abs(want)
-    assert np.mean(rel <= 1e-9) >= 0.8
+    print("runs within 1e-9:", int(np.sum(rel <= 1e-9)), "of", len(rel))
+    assert np.mean(rel <= 1e-9) >= 0.9
     assert np.all(rel <= 1e-2)
 
 

@@ -127,3 +127,37 @@ def test_threshold_command_matches_reference_cli(tmp_path, capsys):
     ref = capsys.readouterr().out.splitlines()
     assert _strip_seconds(ours) == _strip_seconds(ref)
     assert (tmp_path / "ours.pgm").read_bytes() == (tmp_path / "ref.pgm").read_bytes()
+
+
+@pytest.mark.gpu
+def test_bench_command_records_match_reference_cli(tmp_path):
+    """`bench --format json` writes the reference CLI's records (cli.py:166-257): same functions, sizes,
+    seeds, modes and per-run best fitness bit for bit (both modes run the bit-exact keyed stream); only
+    seconds and the worker count (CPU threads there, GPUs here) differ."""
+    import sys
+
+    ref_site = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_site, "protozoa")):
+        pytest.skip("reference not installed in baseline/_ref")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_cli")
+    sys.path.insert(0, ref_site)
+    try:
+        from protozoa import cli as ref_cli
+    finally:
+        sys.path.remove(ref_site)
+    args = ["bench", "--function", "rosenbrock", "--ps", "48", "--dim", "6", "--iters", "30", "--runs", "3",
+            "--seed", "11", "--engine", "both", "--format", "json"]
+    assert cli.main(args + ["--out", str(tmp_path / "ours.json")]) == 0
+    assert ref_cli.main(args + ["--out", str(tmp_path / "ref.json")]) == 0
+    ours = json.loads((tmp_path / "ours.json").read_text())["records"]
+    ref = json.loads((tmp_path / "ref.json").read_text())["records"]
+
+    def strip(recs):
+        out = []
+        for r in recs:
+            r = {k: v for k, v in r.items() if k not in ("avg_seconds", "workers")}
+            r["per_run"] = [{k: v for k, v in p.items() if k != "seconds"} for p in r["per_run"]]
+            out.append(r)
+        return out
+
+    assert strip(ours) == strip(ref)

@@ -419,3 +419,14 @@ def test_ordered_update_equals_gathered_snapshot(pz, name, dim):
         outs.append((out_pos.cpu().numpy(), out_fit.cpu().numpy(), int(warn.item())))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     assert outs[0][2] == outs[1][2]
+
+
+@pytest.mark.parametrize("ps,dim", [(48, 6), (47, 6), (50, 7), (44, 6)])
+def test_batch_shared_memory_just_under_48k(pz, ps, dim):
+    """Batch launches whose dynamic shared memory lands just under 48 KB must still launch (the default
+    limit covers static + dynamic; the attribute is now always set) and a failed launch must not poison
+    the next call's error check."""
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-30.0, 30.0, dim), max_iterations=10, seed=8)
+    res = pz.run(cfg, "rosenbrock")
+    want = oracle.run(ps=ps, dim=dim, max_iterations=10, seed=8, name="rosenbrock", lower=-30.0, upper=30.0)
+    assert np.array_equal(res.trace, want["trace"])
