@@ -363,8 +363,11 @@ def bench_ours(args, rank, world, local):
         "roofline": roofline,
         "roofline_kernels": m["kernels"],
         "clocks": m["clocks"],
-        # per iteration: k_make_keys, k_dr_draw, k_dr_resolve, k_update_group (+ k_cec_eval), CUB sort passes
-        "gpu_launches": (4 + (1 if len(m["kernels"]) > 1 else 0)) * K,
+        # per iteration (profiles/r02_launches_c4.summary.txt): the stable sort = k_make_keys + CUB histogram,
+        # exclusive sum and 8 onesweep passes (11); the coordinator's Dr = k_dr_draw + CUB histogram, exclusive
+        # sum, 3 onesweep passes + k_dr_resolve (7, on the side stream); the update = k_update_group (+ the
+        # evaluation kernel on the split paths).  CUB's kernels are templates compiled into libapo_b200.so.
+        "gpu_launches": (18 + (2 if m["path"] in ("cec_split", "basic_split", "cec_gemm") else 1)) * K,
     }
     if not args.no_suite:
         # the other headline objective, and the memory-bound update on a reference objective (rosenbrock:
