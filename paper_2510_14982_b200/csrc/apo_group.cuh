@@ -242,7 +242,7 @@ template <class Rows>
 __device__ inline void group_phase_a(const IterParams& P, const Rows& R, int i, bool in_dr, double p_dr_i,
                                      const GroupScratch& g, int lane) {
     const int ps = P.ps, dim = P.dim;
-    const Key base = stream_key(P.rng, P.seed, P.key_iteration, (uint64_t)i);
+    const Key base = iteration_key(P, (uint64_t)i);
     const double u_dec = uniform(base, kSlotDecision);
     int op;
     if (in_dr) op = (u_dec < p_dr_i) ? OP_DORMANCY : OP_REPRODUCTION;
@@ -511,7 +511,7 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
     const double f = g.f[p];
     const bool many = MANY && op >= OP_AUTOTROPH;
     Key base{};
-    if (op != OP_AUTOTROPH || many) base = stream_key(P.rng, P.seed, P.key_iteration, (uint64_t)i);
+    if (op != OP_AUTOTROPH || many) base = iteration_key(P, (uint64_t)i);
     if (many) group_extra_pairs(P, R, i, op, base, g, lane);
     const double* xj = staged ? staged + g.rld : R.at_key(sl[op == OP_AUTOTROPH ? 1 : 0]);
     const double* xm = staged ? staged + 2 * g.rld : R.at_key(sl[op >= OP_AUTOTROPH ? 2 : 0]);

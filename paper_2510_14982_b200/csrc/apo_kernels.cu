@@ -752,6 +752,7 @@ int updates_range(const double* positions, const double* fitness, const int32_t*
     P.f_mult = f_mult;
     P.decay = decay;
     P.rng = RNG_KEYED;  // the reference-facing boundary is always oracle mode
+    set_iteration_base(P);
     UpdArgs A{};
     A.P = P;
     A.rank_lo = (int)rank_lo;
@@ -1120,6 +1121,7 @@ int apo_run_iterate(apo_run* r, int64_t n) {
         P.f_mult = r->sched[3 * t + 1];
         P.decay = r->sched[3 * t + 2];
         P.rng = r->rng;
+        set_iteration_base(P);
         cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
         if (r->profile) {
             for (auto& e : ev) {
@@ -1492,6 +1494,7 @@ int apo_shard_update_range(apo_shard* r, int64_t lo, int64_t hi) {
     A.P.f_mult = r->sched[3 * t + 1];
     A.P.decay = r->sched[3 * t + 2];
     A.P.rng = r->rng;
+    set_iteration_base(A.P);
     A.O = r->obj;
     A.pos = r->pos[r->cur];
     A.fit = r->fit[r->cur];

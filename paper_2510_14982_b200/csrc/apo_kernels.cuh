@@ -376,6 +376,7 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
         P.f_mult = A.sched[3 * t + 1];
         P.decay = A.sched[3 * t + 2];
         P.rng = A.rng;
+        set_iteration_base(P);
         const int nxt = cur ^ 1;
         my_min = ~0ull;
         unsigned my_warn = 0;

@@ -32,7 +32,28 @@ struct IterParams {
     double lower, upper, span, eps;
     double p_ah, f_mult, decay;
     int rng;  // RngMode: RNG_KEYED (reference fmix64, oracle mode) or RNG_PHILOX (production)
+    // keyed mode: the (seed, iteration) part of every protozoon's stream base, mix64(mix64(H0^seed)^it)
+    // (rng.py:79-99), hashed once per iteration instead of once per protozoon and call (set_iteration_base)
+    uint64_t base_it;
+    int has_base_it;
 };
+
+__host__ __device__ __forceinline__ void set_iteration_base(IterParams& P) {
+    P.base_it = mix64(mix64(kH0 ^ P.seed) ^ P.key_iteration);
+    P.has_base_it = 1;
+}
+
+// stream_key(P.rng, P.seed, P.key_iteration, individual), with the per-iteration hash reused
+__host__ __device__ __forceinline__ Key iteration_key(const IterParams& P, uint64_t individual) {
+    if (P.rng == RNG_KEYED && P.has_base_it) {
+        Key k;
+        k.mode = RNG_KEYED;
+        k.a = mix64(P.base_it ^ individual);
+        k.b = k.c = 0;
+        return k;
+    }
+    return stream_key(P.rng, P.seed, P.key_iteration, individual);
+}
 
 // Per-warp shared-memory scratch (carved by warp_scratch()).
 struct WarpScratch {
@@ -172,7 +193,7 @@ __device__ inline UpdateResult update_protozoon(const IterParams& P, const ObjDe
     const int ps = P.ps, dim = P.dim;
     const double* x = R.row(i);
     const double fit_i = R.fitness(i);
-    const Key base = stream_key(P.rng, P.seed, P.key_iteration, (uint64_t)i);
+    const Key base = iteration_key(P, (uint64_t)i);
     const double u_dec = uniform(base, kSlotDecision);
 
     int op;
