@@ -789,4 +789,168 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
     }
 }
 
+// The reference's loop (numba_backend.py:96-131) as a running state over a candidate's elements in order.
+struct BasicFold {
+    double s = 0.0, s2 = 0.0, p = 1.0, first = 0.0, prev = 0.0;
+    __device__ __forceinline__ void add(int code, const double* table, int d, double c) {
+        switch (code) {
+        case OBJ_SPHERE: s += c * c; break;
+        case OBJ_BENT_CIGAR:
+            if (d == 0) first = c * c;
+            else s += c * c;
+            break;
+        case OBJ_ELLIPTIC: s += (table[d] * c) * c; break;
+        case OBJ_HGBAT:
+            s += c;
+            s2 += c * c;
+            break;
+        case OBJ_ROSENBROCK:
+            if (d >= 1) {
+                const double a = c - prev * prev;
+                const double b = prev - 1.0;
+                s += 100.0 * (a * a) + b * b;
+            }
+            prev = c;
+            break;
+        default:  // OBJ_GRIEWANK
+            s += c * c;
+            p *= cos_glibc(c / sqrt((double)d + 1.0));
+            break;
+        }
+    }
+    __device__ __forceinline__ double value(int code, int dim) const {
+        switch (code) {
+        case OBJ_SPHERE:
+        case OBJ_ELLIPTIC:
+        case OBJ_ROSENBROCK: return s;
+        case OBJ_BENT_CIGAR: return first + 1e6 * s;
+        case OBJ_HGBAT: return sqrt(fabs(s2 * s2 - s * s)) + (0.5 * s2 + s) / (double)dim + 0.5;
+        default: return 1.0 + s / 4000.0 - p;
+        }
+    }
+};
+
+// Lane-per-protozoon update of a group (the batch kernel's reference objectives at dim <= kLppMaxDim,
+// npairs == 1, rows in shared memory): phase A as above, then each lane builds its own candidate
+// dimension by dimension (the same expressions as group_candidate, numba_backend.py:141-268), folds the
+// reference's objective loop over it as it goes (BasicFold; thresholds and tables on the finished row)
+// and applies the greedy select (numba_backend.py:270-290).  At D <= 8 a warp-per-protozoon pass
+// leaves >= 24 of 32 lanes idle; one warp here carries 32 protozoa, which cuts the batch kernel's
+// instruction count ~2.5x.  Each lane's D-step chain is serial, so this loses above D ~ 8 and for the
+// CEC2022 functions (their quad-DMMA evaluation would serialise 4 passes per warp): measured in
+// profiles/r02_batch_lpp.txt.  OUT_FIXUP by slot only.
+constexpr int kLppMaxDim = 8;
+#ifdef APO_BATCH_CLOCK
+__device__ unsigned long long g_lpp_clk[4];
+#define LPP_CLK(k)                                                                      \
+    do {                                                                                \
+        const long long now_ = clock64();                                               \
+        if (threadIdx.x == 0) atomicAdd(&g_lpp_clk[k], (unsigned long long)(now_ - t_)); \
+        t_ = now_;                                                                      \
+    } while (0)
+#else
+#define LPP_CLK(k) \
+    do {           \
+    } while (0)
+#endif
+template <class Rows>
+__device__ inline void update_group_lpp(const IterParams& P, const ObjDesc& O, const Rows& R, int i0, int n,
+                                        const unsigned* in_dr_bits, const double* p_dr, double* out_rows,
+                                        double* out_fit, const GroupScratch& g, int lane,
+                                        unsigned long long& my_min, unsigned& my_warn) {
+    const int dim = P.dim;
+    const bool live = lane < n;
+#ifdef APO_BATCH_CLOCK
+    long long t_ = clock64();
+#endif
+    if (live) {
+        const int r0 = i0 - 1 + lane;
+        const bool dr = ((in_dr_bits[r0 >> 5] >> (r0 & 31)) & 1u) != 0;
+        group_phase_a(P, R, i0 + lane, dr, dr ? p_dr[r0] : 0.0, g, lane);
+    }
+    LPP_CLK(0);
+    bool ok = true;
+    double nf = 0.0;
+    int own_key = 0;
+    double* dst = nullptr;
+    const double* x = nullptr;
+    if (live) {
+        const int i = i0 + lane;
+        const int op = g.op[lane];
+        const int* sl = g.slot + 4 * lane;
+        own_key = sl[0];
+        x = R.at_key(own_key);
+        const double* xj = R.at_key(sl[op == OP_AUTOTROPH ? 1 : 0]);
+        const double* xm = R.at_key(sl[op >= OP_AUTOTROPH ? 2 : 0]);
+        const double* xp = R.at_key(sl[op >= OP_AUTOTROPH ? 3 : 0]);
+        dst = out_rows + (size_t)R.slot_of(own_key) * P.ld;
+        Key base{};
+        if (op != OP_AUTOTROPH) base = iteration_key(P, (uint64_t)i);
+        const double f = g.f[lane], w0 = g.w[lane], sgn = g.sgn[lane];
+        const unsigned* mb = g.bits + lane * g.words;
+        const bool basic = O.code <= OBJ_GRIEWANK;
+        BasicFold bf;
+#pragma unroll 2
+        for (int d = 0; d < dim; d++) {
+            const double xd = x[d];
+            const double m = ((mb[d >> 5] >> (d & 31)) & 1u) ? 1.0 : 0.0;
+            double cv;
+            if (op == OP_DORMANCY) {
+                cv = P.lower + uniform(base, kVectorBase + (uint64_t)d) * P.span;
+            } else if (op == OP_REPRODUCTION) {
+                const double off = P.lower + uniform(base, kVectorBase + (uint64_t)d) * P.span;
+                cv = xd + (f * off) * m;
+            } else {
+                double acc = 0.0;
+                acc = acc + w0 * (xm[d] - xp[d]);
+                const double ep = acc;
+                double direction;
+                if (op == OP_AUTOTROPH) {
+                    direction = (xj[d] - xd) + ep;
+                } else {
+                    const double uv = uniform(base, kVectorBase + (uint64_t)d);
+                    direction = ((1.0 + (sgn * uv) * P.decay) * xd - xd) + ep;
+                }
+                cv = xd + (f * direction) * m;
+            }
+            const double c = clampv(cv, P.lower, P.upper);
+            ok = ok && isfinite(c);
+            dst[d] = c;
+            if (basic) bf.add(O.code, O.table, d, c);
+        }
+        if (basic) {
+            nf = bf.value(O.code, dim);
+        } else if (O.code == OBJ_OTSU_ML || O.code == OBJ_KAPUR_ML) {
+            nf = threshold_ml(O.code, dst, dim, O.table);
+        } else {  // OBJ_TABLE
+            long long idx = (long long)floor(dst[0] + 0.5);
+            if (idx < 0) idx = 0;
+            if (idx > O.table_len - 1) idx = O.table_len - 1;
+            nf = O.table[idx];
+        }
+    }
+    LPP_CLK(1);
+    if (live) {
+        const int own = R.slot_of(own_key);
+        const double fit_i = R.fit_at(own);
+        double kept = fit_i;
+        bool acc = false, warned = false;
+        if (ok && isfinite(nf)) {
+            acc = nf < fit_i;
+            if (acc) kept = nf;
+        } else {
+            warned = true;
+        }
+        out_fit[own] = kept;
+        if (!acc)
+            for (int d = 0; d < dim; d++) dst[d] = x[d];
+        const unsigned long long k = sort_key(kept);
+        my_min = k < my_min ? k : my_min;
+        my_warn += warned ? 1u : 0u;
+    }
+    __syncwarp();
+    LPP_CLK(3);
+}
+#undef LPP_CLK
+
 }  // namespace apo

@@ -6,6 +6,9 @@
 // and reaches the templates through the pick_* getters below.
 #pragma once
 #include <cstdint>
+#ifdef APO_BATCH_CLOCK
+#include <cstdio>
+#endif
 #include "apo_group.cuh"
 #include "apo_update.cuh"
 
@@ -192,6 +195,8 @@ struct BatchArgs {
     // none is left, so an SM that drew cheap runs takes more; else CTA b does run b
     const int* run_order;
     unsigned* run_counter;
+    int lpp;        // npairs == 1: lane-per-protozoon groups at dim <= kLppMaxDim (update_group_lpp)
+    int lpp_group;  // protozoa per warp on that path
 };
 
 struct BatchLayout {
@@ -315,6 +320,20 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
     }
     unsigned warn_total = 0;
     int cur = 0;
+#ifdef APO_BATCH_CLOCK
+    long long clk_sum[6] = {0, 0, 0, 0, 0, 0};
+    long long clk_prev = clock64();
+#define CLK(k)                                       \
+    do {                                             \
+        const long long now_ = clock64();            \
+        clk_sum[k] += now_ - clk_prev;               \
+        clk_prev = now_;                             \
+    } while (0)
+#else
+#define CLK(k) \
+    do {       \
+    } while (0)
+#endif
     for (int t = 0; t < A.n_iters; t++) {
         // 1. stable sort by fitness, ties by previous rank (core.py:504-513): each rank is a count of
         //    smaller keys, S lanes per element (S a power of two, the counts folded by shuffles); the
@@ -354,12 +373,14 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
             }
         }
         __syncthreads();
+        CLK(0);
         for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) {
             order[newrank[sl]] = sl;
             rankof[sl] = newrank[sl];
         }
         if (!dr_overlap && warp == 0) coordinator();
         __syncthreads();
+        CLK(1);
         // 3. fused updates
         IterParams P;
         P.seed = seed;
@@ -382,13 +403,27 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
         unsigned my_warn = 0;
         if constexpr (MAXC >= 0) {
             const OrderedSlots R{pos[cur], fit[cur], order, ld};
-            const int G = min(32, (ps + nwarps - 1) / nwarps);
+            const bool lpp = MAXC == 1 && A.lpp && O.code < OBJ_CEC_BASE && dim <= kLppMaxDim;
+            const int G = lpp ? min(32, max(A.lpp_group, (ps + nwarps - 1) / nwarps))
+                              : min(32, (ps + nwarps - 1) / nwarps);
+#ifdef APO_BATCH_CLOCK
+            const long long own0 = clock64();
+#endif
             for (int q = warp; q * G < ps; q += nwarps) {
                 const int i0 = q * G + 1;
-                update_group<MAXC, OUT_FIXUP, KIND_ANY>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr, pos[nxt],
-                                              fit[nxt], true, nullptr, nullptr, nullptr, g, lane, my_min, my_warn);
+                if (MAXC == 1 && lpp)
+                    update_group_lpp(P, O, R, i0, min(G, ps - q * G), cs.bits, A.p_dr, pos[nxt], fit[nxt], g, lane,
+                                     my_min, my_warn);
+                else
+                    update_group<MAXC, OUT_FIXUP, KIND_ANY>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr,
+                                                            pos[nxt], fit[nxt], true, nullptr, nullptr, nullptr, g,
+                                                            lane, my_min, my_warn);
             }
+#ifdef APO_BATCH_CLOCK
+            clk_sum[5] += clock64() - own0;
+#endif
             __syncthreads();
+            CLK(2);
             for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) keys[sl] = sort_key(fit[nxt][sl]);
         } else {
             const OrderedRows R{pos[cur], fit[cur], order, ld};
@@ -416,6 +451,7 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
             red_warn[warp] = my_warn;
         }
         __syncthreads();
+        CLK(3);
         if (threadIdx.x == 0) {
             unsigned long long m = ~0ull;
             for (int k = 0; k < nwarps; k++) {
@@ -426,7 +462,18 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
         }
         cur = nxt;
         __syncthreads();
+        CLK(4);
     }
+#ifdef APO_BATCH_CLOCK
+    if (threadIdx.x == 0 || threadIdx.x == 32 * (nwarps - 1))
+        printf("batch clock run %d thread %d: sort %lld order+dr %lld update %lld reduce %lld tail %lld own-update %lld (cycles/iter)\n",
+               run, (int)threadIdx.x, clk_sum[0] / A.n_iters, clk_sum[1] / A.n_iters, clk_sum[2] / A.n_iters,
+               clk_sum[3] / A.n_iters, clk_sum[4] / A.n_iters, clk_sum[5] / A.n_iters);
+    if (threadIdx.x == 0)
+        printf("lpp warp 0 (cycles/iter): phaseA %llu cand+fold %llu select %llu\n", g_lpp_clk[0] / A.n_iters,
+               g_lpp_clk[1] / A.n_iters, g_lpp_clk[3] / A.n_iters);
+#endif
+#undef CLK
     // outputs in reference row order (row r = order[r])
     if (threadIdx.x == 0) {
         int best = 0;
@@ -693,46 +740,6 @@ struct BasicEvalArgs {
 
 __host__ __device__ inline bool basic_split_code(int code) { return code >= OBJ_SPHERE && code <= OBJ_GRIEWANK; }
 
-// The reference's loop (numba_backend.py:96-131) as a running state over a candidate's elements in order.
-struct BasicFold {
-    double s = 0.0, s2 = 0.0, p = 1.0, first = 0.0, prev = 0.0;
-    __device__ __forceinline__ void add(int code, const double* table, int d, double c) {
-        switch (code) {
-        case OBJ_SPHERE: s += c * c; break;
-        case OBJ_BENT_CIGAR:
-            if (d == 0) first = c * c;
-            else s += c * c;
-            break;
-        case OBJ_ELLIPTIC: s += (table[d] * c) * c; break;
-        case OBJ_HGBAT:
-            s += c;
-            s2 += c * c;
-            break;
-        case OBJ_ROSENBROCK:
-            if (d >= 1) {
-                const double a = c - prev * prev;
-                const double b = prev - 1.0;
-                s += 100.0 * (a * a) + b * b;
-            }
-            prev = c;
-            break;
-        default:  // OBJ_GRIEWANK
-            s += c * c;
-            p *= cos_glibc(c / sqrt((double)d + 1.0));
-            break;
-        }
-    }
-    __device__ __forceinline__ double value(int code, int dim) const {
-        switch (code) {
-        case OBJ_SPHERE:
-        case OBJ_ELLIPTIC:
-        case OBJ_ROSENBROCK: return s;
-        case OBJ_BENT_CIGAR: return first + 1e6 * s;
-        case OBJ_HGBAT: return sqrt(fabs(s2 * s2 - s * s)) + (0.5 * s2 + s) / (double)dim + 0.5;
-        default: return 1.0 + s / 4000.0 - p;
-        }
-    }
-};
 
 // Greedy select of row r (numba_backend.py:270-290), rejected rows restored in dense mode.
 template <bool SEL>

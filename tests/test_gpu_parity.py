@@ -250,6 +250,22 @@ def test_persistent_batch_matches_oracle_runs(pz):
         assert np.array_equal(part.trace, big.trace[k0:k0 + 12])
 
 
+@pytest.mark.parametrize("ps,dim", [(2, 1), (33, 3), (100, 5), (700, 4), (64, 8), (50, 9)])
+def test_batch_lane_per_protozoon_groups_match_oracle(pz, ps, dim):
+    """dim <= 8 (update_group_lpp: one lane per protozoon, 32 per warp, the fitness folded as the candidate
+    is built) and dim = 9 (warp per protozoon) against the oracle's run loop, bit-exact; every reference
+    objective, the default CTA and a 2-warp CTA (several groups per warp)."""
+    names = ["sphere", "bent_cigar", "high_conditioned_elliptic", "hgbat", "rosenbrock", "griewank"]
+    names = [n for n in names if pz.get_objective(n).min_dim <= dim]
+    seeds = [11 * k + dim for k in range(len(names))]
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-20.0, 30.0, dim), max_iterations=25)
+    want, _ = oracle.run_many(names, seeds, ps=ps, dim=dim, max_iterations=25, lower=-20.0, upper=30.0)
+    for threads in (0, 64):
+        res = pz.run_batch(cfg, names, seeds, want_trace=True, threads_per_run=threads)
+        assert np.array_equal(res.best_fitness, want), threads
+        assert np.array_equal(res.trace[:, -1], want), threads
+
+
 def test_batch_launch_shapes_agree(pz):
     """apo_run_batch_shaped: any CTA size gives the same runs (rank counts, group sizes and the Dr warp
     depend on it, the results must not); out-of-range sizes are rejected."""
