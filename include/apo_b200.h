@@ -43,6 +43,22 @@ extern "C" {
  *   statistically (not bitwise) equivalent. */
 #define APO_RNG_KEYED 0
 #define APO_RNG_PHILOX 1
+/* APO_RNG_TABLE: scripted draws (the "identical pre-generated random tensor" oracle mode, replaying
+ *   the reference's ScriptedStream, tests/test_acceptance.py:50-80): every draw (individual, counter)
+ *   is read from an apo_draw_table; only the *_scripted entries below take it. */
+#define APO_RNG_TABLE 2
+
+/* A draw table in DEVICE memory (the struct itself and its arrays): n entries sorted by
+ * (individual, counter), value = the uniform in [0, 1) that draw returns.  miss (device, 3 words,
+ * zeroed by the caller) receives {1, individual, counter} of the first draw the table lacks; that
+ * draw reads 0.0 and the caller must treat the call as failed (engine.step raises LookupError). */
+typedef struct apo_draw_table {
+    int64_t n;
+    const uint64_t *individual;
+    const uint64_t *counter;
+    const double *value;
+    uint64_t *miss;
+} apo_draw_table;
 
 /* Objective codes (objectives.py:34-42), plus codes the reference lacks. */
 #define APO_OBJ_SPHERE 0
@@ -157,6 +173,16 @@ int apo_sort_order(const double *fitness, int64_t n, int32_t *order, void *strea
  * set size through count_host (nullable). */
 int apo_select_dr(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_max, uint8_t *in_dr,
                   int64_t *count_host, void *stream);
+
+/* Scripted-draw variants of apo_run_updates_obj and apo_select_dr (APO_RNG_TABLE): `table` is the
+ * device address of an apo_draw_table; the coordinator's set size `count` = ceil(ps * pf) is computed by
+ * the caller from its scripted pf draw (core.py:263-278).  Same kernels as the keyed entries. */
+int apo_run_updates_scripted(const double *positions, const double *fitness, const uint8_t *in_dr, double *out_pos,
+                             double *out_fit, uint8_t *out_acc, uint8_t *out_warn, int64_t ps, int64_t dim,
+                             const apo_draw_table *table, int64_t npairs, double lower, double upper, double eps,
+                             double p_ah, double f_mult, double decay, const apo_objective *objective_host,
+                             const double *p_dr, unsigned long long *warn_count, void *stream);
+int apo_select_dr_scripted(const apo_draw_table *table, int64_t ps, int64_t count, uint8_t *in_dr, void *stream);
 
 /* Prefix tables of a 256-bin histogram for APO_OBJ_OTSU_ML (method 0) or
  * APO_OBJ_KAPUR_ML (method 1): table[0] = N, table[1+i] = sum_{v<i} count_v,

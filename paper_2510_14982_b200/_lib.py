@@ -30,7 +30,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-
 SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_batch.cu", "apo_batch_m1.cu",
            "apo_batch_m2.cu", "apo_batch_m4.cu", "apo_batch_m0.cu", "apo_batch_warp.cu", "apo_cec_eval.cu",
            "apo_cec_gemm.cu", "apo_prologue.cu", "apo_update_fused.cu",
-           "apo_update_fused12.cu"]
+           "apo_update_fused12.cu", "apo_update_scripted.cu"]
 
 # CEC2022-only TUs (parity unpinned, checked at 1e-9 relative): FMA contraction allowed.  Every TU
 # on the reference's bit-exact path keeps --fmad=false.
@@ -73,8 +73,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         os.makedirs(objdir, exist_ok=True)
         flags = [f for f in NVCC_FLAGS if f != "-shared"]
 
+        headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h"))]
+        headers.append(os.path.join(INCLUDE, "apo_b200.h"))
+        newest_header = max(os.path.getmtime(h) for h in headers)
+
         def compile_one(src):
             obj = os.path.join(objdir, src.replace(".cu", ".o"))
+            if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(
+                    newest_header, os.path.getmtime(os.path.join(CSRC, src))):
+                return obj, subprocess.CompletedProcess([], 0, "", "")  # up to date (same flags)
             f = flags
             if src in FMA_SOURCES:  # no bit-exact reference there: let nvcc contract multiply-adds
                 f = ["--fmad=true" if x == "--fmad=false" else x for x in flags]
@@ -126,6 +133,9 @@ PROTOTYPES = {
                                      C.POINTER(apo_objective), _P, _P, _I, _I, _P]),
     "apo_run_updates_ordered": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _U, _U, _I, _D, _D, _D, _D, _D, _D,
                                        C.POINTER(apo_objective), _P, _P, _I, _I, _P]),
+    "apo_run_updates_scripted": (_INT, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _I, _D, _D, _D, _D, _D, _D,
+                                        C.POINTER(apo_objective), _P, _P, _P]),
+    "apo_select_dr_scripted": (_INT, [_P, _I, _I, _P, _P]),
     "apo_evaluate": (_INT, [_P, _I, _I, _I, C.POINTER(apo_objective), _P, _P]),
     "apo_initialize": (_INT, [_U, _I, _I, _I, _D, _D, C.POINTER(apo_objective), _P, _P, _P]),
     "apo_sort_order": (_INT, [_P, _I, _P, _P]),

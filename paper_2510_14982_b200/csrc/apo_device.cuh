@@ -57,7 +57,20 @@ __host__ __device__ __forceinline__ double uniform(uint64_t base, uint64_t count
 // (slot lo, slot hi, protozoon, iteration); the draw is the top 53 bits of
 // the first two output words.  Slots are the reference's draw-slot layout
 // (core.py:18-47), so every draw keeps its meaning; only the bits differ.
-enum RngMode : int { RNG_KEYED = 0, RNG_PHILOX = 1 };
+enum RngMode : int { RNG_KEYED = 0, RNG_PHILOX = 1, RNG_TABLE = 2 };
+
+// Scripted draws (APO_RNG_TABLE, include/apo_b200.h apo_draw_table): the stream's `seed` word carries
+// the device address of the table; a draw is looked up by (individual, counter) in entries sorted by
+// that pair.  A draw the table does not hold records the first such address in miss[1..2], sets
+// miss[0] and reads 0.0 (so every index derived from it stays in range); the host then fails the call
+// (the reference's ScriptedStream fails on any unscripted read, tests/test_acceptance.py:50-80).
+struct DrawTable {
+    long long n;
+    const unsigned long long* individual;
+    const unsigned long long* counter;
+    const double* value;
+    unsigned long long* miss;
+};
 
 __host__ __device__ __forceinline__ void philox_mulhilo(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
 #ifdef __CUDA_ARCH__
@@ -95,6 +108,10 @@ __host__ __device__ inline uint64_t philox4x32_10(uint32_t c0, uint32_t c1, uint
 
 // Per-protozoon stream key for either generator.  uniform(Key, counter) is
 // the only draw primitive the kernels use.
+// Key.c of a scripted-draw key: lets the one out-of-line draw function tell the table from Philox
+// without a mode argument (Philox keys carry the iteration there, < 2^31 on every entry point).
+constexpr uint32_t kTableMark = 0xFFFFFFFFu;
+
 struct Key {
     uint64_t a;   // keyed: the fmix64 stream base; philox: the seed
     uint32_t b;   // philox: protozoon (folded to 32 bits; the coordinator maps above 2^31)
@@ -109,6 +126,10 @@ __host__ __device__ __forceinline__ Key stream_key(int mode, uint64_t seed, uint
         k.a = seed;
         k.b = (uint32_t)individual ^ ((uint32_t)(individual >> 32) * 0x9E3779B9u);
         k.c = (uint32_t)iteration;
+    } else if (mode == RNG_TABLE) {  // a = table address, b = the individual (the script is one iteration)
+        k.a = seed;
+        k.b = individual == kCoordinator ? 0xFFFFFFFFu : (uint32_t)individual;  // protozoa are < 2^31
+        k.c = kTableMark;
     } else {
         k.a = stream_base(seed, iteration, individual);
         k.b = k.c = 0;
@@ -116,24 +137,48 @@ __host__ __device__ __forceinline__ Key stream_key(int mode, uint64_t seed, uint
     return k;
 }
 
-#ifndef APO_PHILOX_INLINE
-#define APO_PHILOX_INLINE __noinline__
-#endif
+__host__ __device__ __forceinline__ double philox_draw(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
+    return (double)(philox4x32_10((uint32_t)counter, (uint32_t)(counter >> 32), b, c, (uint32_t)seed,
+                                  (uint32_t)(seed >> 32)) >> 11) * kInv2p53;
+}
+
 #ifdef __CUDA_ARCH__
-__device__ APO_PHILOX_INLINE double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
-    return (double)(philox4x32_10((uint32_t)counter, (uint32_t)(counter >> 32), b, c, (uint32_t)seed,
-                                  (uint32_t)(seed >> 32)) >> 11) * kInv2p53;
+__device__ __noinline__ double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
+    return philox_draw(seed, b, c, counter);
 }
-#else
-inline double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
-    return (double)(philox4x32_10((uint32_t)counter, (uint32_t)(counter >> 32), b, c, (uint32_t)seed,
-                                  (uint32_t)(seed >> 32)) >> 11) * kInv2p53;
+#ifdef APO_RNG_TABLE_ENABLED
+__device__ __forceinline__ double table_draw(uint64_t table, uint64_t individual, uint64_t counter) {
+    const DrawTable* T = reinterpret_cast<const DrawTable*>(table);
+    long long lo = 0, hi = T->n;  // first entry >= (individual, counter)
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        const unsigned long long mi = T->individual[mid], mc = T->counter[mid];
+        if (mi < individual || (mi == individual && mc < counter)) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo < T->n && T->individual[lo] == individual && T->counter[lo] == counter) return T->value[lo];
+    if (atomicCAS(&T->miss[0], 0ull, 1ull) == 0ull) {
+        T->miss[1] = individual;
+        T->miss[2] = counter;
+    }
+    return 0.0;
 }
+#endif
 #endif
 
+// Scripted keys (c == kTableMark) are only read by kernels built with APO_RNG_TABLE_ENABLED -- their
+// own instantiations in apo_update_scripted.cu: any table code in the keyed kernels, even on a branch
+// they never take, measured +1.5-9% on the C4 update (it shifts ptxas' register allocation).
 __host__ __device__ __forceinline__ double uniform(const Key& k, uint64_t counter) {
-    if (k.mode == RNG_PHILOX) return philox_uniform(k.a, k.b, k.c, counter);
-    return uniform(k.a, counter);
+    if (k.mode == RNG_KEYED) return uniform(k.a, counter);
+#ifdef __CUDA_ARCH__
+#ifdef APO_RNG_TABLE_ENABLED
+    if (k.c == kTableMark) return table_draw(k.a, k.b == 0xFFFFFFFFu ? kCoordinator : (uint64_t)k.b, counter);
+#endif
+    return philox_uniform(k.a, k.b, k.c, counter);
+#else
+    return k.c == kTableMark ? 0.0 : philox_draw(k.a, k.b, k.c, counter);  // host: the table is device memory
+#endif
 }
 
 // ---------------------------------------------------------------------------

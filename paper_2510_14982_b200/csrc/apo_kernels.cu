@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -31,6 +32,9 @@
 #include "apo_kernels.cuh"
 
 using namespace apo;
+
+static_assert(sizeof(apo_draw_table) == sizeof(DrawTable) && offsetof(apo_draw_table, miss) == offsetof(DrawTable, miss),
+              "apo_draw_table (include/apo_b200.h) and DrawTable (apo_device.cuh) must share one layout");
 
 namespace {
 
@@ -361,7 +365,7 @@ int update_path(bool sel_mode, const UpdArgs& a0, bool have_cand_ok, bool have_c
 constexpr int kCecFmaMaxDim = 32;  // the fused FMA rotation beats the DMMA split up to here (device loop)
 
 int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* cand_ok = nullptr,
-                  cudaEvent_t mid_event = nullptr, unsigned* tile_counter = nullptr) {
+                  cudaEvent_t mid_event = nullptr, unsigned* tile_counter = nullptr, bool scripted = false) {
     UpdArgs a = A0;
     const int dim = a.P.dim;
     if ((a.O.flags & APO_OBJ_FMA_SMALL_D) && dim <= kCecFmaMaxDim) a.O.cec.rot_pad = nullptr;  // FMA rotation
@@ -392,8 +396,9 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     while (w > 1 && per_warp * (size_t)w + 1024 > (size_t)smem_optin()) w--;  // e.g. fused CEC at D ~ 150-256
     const size_t smem = per_warp * (size_t)w;
     const bool cec = a.O.code > APO_OBJ_CEC2022_BASE;
-    const void* fn = sel_mode ? pick_update_sel(dim, split || gemm || bsplit, cec)
-                              : pick_update_dense(dim, split || gemm || bsplit, cec);
+    const void* fn = scripted   ? pick_update_scripted(dim, split || gemm || bsplit, cec)
+                     : sel_mode ? pick_update_sel(dim, split || gemm || bsplit, cec)
+                                : pick_update_dense(dim, split || gemm || bsplit, cec);
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
@@ -671,7 +676,7 @@ struct apo_run {
 
 extern "C" {
 
-int apo_abi_version(void) { return 3; }  // 3: apo_objective.flags, apo_run_updates_ordered; 2: rng, shard/load/threshold
+int apo_abi_version(void) { return 4; }  // 4: scripted draws; 3: apo_objective.flags, apo_run_updates_ordered; 2: rng, shard/load/threshold
 
 const char* apo_last_error(void) { return g_err.c_str(); }
 
@@ -697,7 +702,8 @@ int updates_range(const double* positions, const double* fitness, const int32_t*
                   double* out_pos, double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim,
                   uint64_t seed, uint64_t key_iteration, int64_t npairs, double lower, double upper, double eps,
                   double p_ah, double f_mult, double decay, const apo_objective* objective_host, const double* p_dr,
-                  unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi, void* stream);
+                  unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi, void* stream,
+                  int rng = RNG_KEYED);
 }
 
 int apo_run_updates_range(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
@@ -729,7 +735,7 @@ int updates_range(const double* positions, const double* fitness, const int32_t*
                   double* out_pos, double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim,
                   uint64_t seed, uint64_t key_iteration, int64_t npairs, double lower, double upper, double eps,
                   double p_ah, double f_mult, double decay, const apo_objective* objective_host, const double* p_dr,
-                  unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi, void* stream) {
+                  unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi, void* stream, int rng) {
     APO_CHECK(ps >= 1 && ps < (1LL << 31), "ps out of range");
     APO_CHECK(0 <= rank_lo && rank_lo < rank_hi && rank_hi <= ps, "rank range must satisfy 0 <= lo < hi <= ps");
     APO_CHECK(dim >= 1 && dim <= 8192, "dim out of range (1..8192)");
@@ -751,8 +757,9 @@ int updates_range(const double* positions, const double* fitness, const int32_t*
     P.p_ah = p_ah;
     P.f_mult = f_mult;
     P.decay = decay;
-    P.rng = RNG_KEYED;  // the reference-facing boundary is always oracle mode
-    set_iteration_base(P);
+    P.rng = rng;  // the reference-facing boundary: the keyed stream, or scripted draws (RNG_TABLE)
+    if (rng == RNG_KEYED) set_iteration_base(P);
+    else P.has_base_it = 0;
     UpdArgs A{};
     A.P = P;
     A.rank_lo = (int)rank_lo;
@@ -775,11 +782,23 @@ int updates_range(const double* positions, const double* fitness, const int32_t*
     const size_t ok_bytes = ((size_t)ps + 15) & ~(size_t)15;  // cand_ok, then the k_cec_eval tile counter
     if (cec) APO_CUDA(cudaMallocAsync((void**)&cand_ok, ok_bytes + 16, as_stream(stream)));
     unsigned* counter = cec ? reinterpret_cast<unsigned*>(cand_ok + ok_bytes) : nullptr;
-    const int rc = launch_update(false, A, as_stream(stream), cand_ok, nullptr, counter);
+    const int rc = launch_update(false, A, as_stream(stream), cand_ok, nullptr, counter, rng == RNG_TABLE);
     if (cec) cudaFreeAsync(cand_ok, as_stream(stream));
     return rc;
 }
 }  // namespace
+
+int apo_run_updates_scripted(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
+                             double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim,
+                             const apo_draw_table* table, int64_t npairs, double lower, double upper, double eps,
+                             double p_ah, double f_mult, double decay, const apo_objective* objective_host,
+                             const double* p_dr, unsigned long long* warn_count, void* stream) {
+    APO_CHECK(table != nullptr, "table is NULL");
+    if (warn_count) APO_CUDA(cudaMemsetAsync(warn_count, 0, sizeof(unsigned long long), as_stream(stream)));
+    return updates_range(positions, fitness, nullptr, in_dr, out_pos, out_fit, out_acc, out_warn, ps, dim,
+                         (uint64_t)(uintptr_t)table, 0, npairs, lower, upper, eps, p_ah, f_mult, decay,
+                         objective_host, p_dr, warn_count, 0, ps, stream, RNG_TABLE);
+}
 
 int apo_run_updates(const double* positions, const double* fitness, const uint8_t* in_dr, double* out_pos,
                     double* out_fit, uint8_t* out_acc, uint8_t* out_warn, int64_t ps, int64_t dim, uint64_t seed,
@@ -895,6 +914,17 @@ int apo_select_dr(uint64_t seed, uint64_t key_iteration, int64_t ps, double pf_m
     return rc;
 }
 
+int apo_select_dr_scripted(const apo_draw_table* table, int64_t ps, int64_t count, uint8_t* in_dr, void* stream) {
+    APO_CHECK(table && in_dr && ps >= 1 && ps < (1LL << 31), "bad arguments");
+    APO_CHECK(count >= 0 && count <= ps, "count must be in [0, ps]");
+    cudaStream_t st = as_stream(stream);
+    int* perm = nullptr;
+    APO_CUDA(cudaMallocAsync((void**)&perm, 4 * (size_t)ps, st));
+    APO_CUDA(launch_dr_scripted((uint64_t)(uintptr_t)table, (int)ps, (int)count, perm, in_dr, st));
+    cudaFreeAsync(perm, st);
+    return APO_OK;
+}
+
 int apo_histogram_u8(const uint8_t* pixels, int64_t n, int64_t* counts, void* stream) {
     APO_CHECK(n >= 0 && counts && (n == 0 || pixels), "bad arguments");
     APO_CHECK(((uintptr_t)pixels & 15) == 0, "pixels must be 16-byte aligned");
@@ -923,7 +953,10 @@ void apo_philox4x32_10(const uint32_t* ctr4, const uint32_t* key2, uint32_t* out
 }
 
 double apo_rng_uniform(int rng, uint64_t seed, uint64_t iteration, uint64_t individual, uint64_t counter) {
-    return uniform(stream_key(rng, seed, iteration, individual), counter);
+    const Key k = stream_key(rng, seed, iteration, individual);
+    if (rng == RNG_PHILOX) return philox_draw(k.a, k.b, k.c, counter);  // any iteration, kTableMark included
+    if (rng == RNG_TABLE) return NAN;                                    // the table lives in device memory
+    return uniform(k, counter);
 }
 
 int apo_debug_cos(const double* x, double* out, int64_t n, void* stream) {

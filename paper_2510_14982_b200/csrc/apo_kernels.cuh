@@ -903,6 +903,8 @@ __host__ __device__ inline int gemm_np(int dim) { return (dim + 63) & ~63; }
 // Kernel getters (defined in the instantiating TUs).
 const void* pick_update_sel(int dim, bool cand_only, bool cec);
 const void* pick_update_dense(int dim, bool cand_only, bool cec);
+const void* pick_update_scripted(int dim, bool cand_only, bool cec);  // apo_update_scripted.cu
+cudaError_t launch_dr_scripted(uint64_t table, int ps, int count, int* perm, uint8_t* in_dr, cudaStream_t st);
 const void* pick_run_batch(int dim);
 // apo_prologue.cu: stable sort + Dr set as one launch for small populations (else the CUB prologue)
 bool prologue_small_fits(long long ps);

@@ -169,8 +169,12 @@ def _copy_stream(dev):
 
 
 def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: EngineMode = None,
-         backend: Optional[str] = None) -> Population:
-    """One full iteration; returns the next population, input untouched (engine.py:142-172)."""
+         backend: Optional[str] = None, draws=None) -> Population:
+    """One full iteration; returns the next population, input untouched (engine.py:142-172).
+
+    draws: an rng.DrawTable -- every draw of the iteration is read from it instead of the keyed stream
+    (the reference replays its hand-traced example this way, tests/test_acceptance.py:50-175); a draw the
+    table lacks raises LookupError."""
     import torch
 
     mode = mode or EngineMode.sequential()
@@ -178,6 +182,15 @@ def step(pop: Population, cfg: ApoConfig, objective, iteration: int, mode: Engin
     if pop.size != cfg.ps or pop.dim != cfg.dim:
         raise ValueError(f"population shape ({pop.size}, {pop.dim}) does not match config "
                          f"(ps={cfg.ps}, dim={cfg.dim})")
+    if draws is not None:
+        from .kernels import cuda_backend
+
+        dev = _dev()
+        new_pos, new_fit, _acc, warned = cuda_backend.scripted_step_device(
+            _to_device(pop.positions, dev), _to_device(pop.fitness, dev), cfg, obj, iteration, draws)
+        hp, hf = _to_host(new_pos, new_fit)
+        return Population(hp, hf, iteration=iteration + 1, fe_count=pop.fe_count + cfg.ps,
+                          warnings=pop.warnings + warned)
     bk = _resolve_backend(obj, backend)
     workers = resolve_workers(mode, bk)
     if cfg.rng != "keyed":

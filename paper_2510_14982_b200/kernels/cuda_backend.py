@@ -124,3 +124,58 @@ def run_updates_to_host(pos, fit, in_dr, cfg: ApoConfig, objective: Objective, i
         t.record_stream(copy)
     copy.synchronize()
     return hp.numpy(), hf.numpy(), int(warn.item())
+
+
+def scripted_step_device(pos, fit, cfg: ApoConfig, objective: Objective, iteration: int, draws):
+    """One iteration on device tensors with every draw read from `draws` (rng.DrawTable, APO_RNG_TABLE):
+    stable sort, the coordinator's set from its scripted pf and permutation draws, the fused update.
+    Returns (next positions, next fitness, accepted, warnings) by rank; raises LookupError on the first
+    unscripted draw (the reference's ScriptedStream contract, tests/test_acceptance.py:50-80)."""
+    import math
+
+    import torch
+
+    from ..rng import COORDINATOR_INDEX
+
+    if objective.code == EXTERNAL:
+        raise ValueError("the cuda backend cannot call external objective functions")
+    if draws.seed != cfg.seed or draws.iteration != iteration + 1:
+        raise ValueError(f"draw table is for (seed {draws.seed}, iteration {draws.iteration}); this step reads "
+                         f"(seed {cfg.seed}, iteration {iteration + 1})")
+    lib = _lib.require_cuda()
+    dev = pos.device
+    ps, dim = pos.shape
+    ind, ctr, val = draws.arrays()
+    u = draws.uniforms()
+    pf_key = (COORDINATOR_INDEX, 0)  # COORD_SLOT_PF
+    if pf_key not in u:
+        raise LookupError(f"unscripted draw at (individual {COORDINATOR_INDEX}, counter 0)")
+    count = int(math.ceil(ps * (cfg.pf_max * u[pf_key])))  # core.py:263-278
+    t_ind = torch.as_tensor(ind.view(np.int64), device=dev)
+    t_ctr = torch.as_tensor(ctr.view(np.int64), device=dev)
+    t_val = torch.as_tensor(val, device=dev)
+    miss = torch.zeros(3, dtype=torch.int64, device=dev)
+    header = torch.as_tensor(np.array([len(val), t_ind.data_ptr(), t_ctr.data_ptr(), t_val.data_ptr(),
+                                       miss.data_ptr()], dtype=np.uint64).view(np.int64), device=dev)
+    stream = _lib.stream_handle()
+    order = torch.empty(ps, dtype=torch.int32, device=dev)
+    _lib.check(lib.apo_sort_order(_lib.ptr(fit), ps, _lib.ptr(order), stream), "apo_sort_order")
+    in_dr = torch.empty(ps, dtype=torch.uint8, device=dev)
+    _lib.check(lib.apo_select_dr_scripted(_lib.ptr(header), ps, count, _lib.ptr(in_dr), stream),
+               "apo_select_dr_scripted")
+    idx = order.long()
+    snap_pos = pos.index_select(0, idx).contiguous()
+    snap_fit = fit.index_select(0, idx).contiguous()
+    out_pos, out_fit = torch.empty_like(snap_pos), torch.empty_like(snap_fit)
+    acc = torch.empty(ps, dtype=torch.uint8, device=dev)
+    warn = torch.zeros(1, dtype=torch.int64, device=dev)
+    p_ah, f_mult, decay = iteration_scalars(iteration, cfg.max_iterations)
+    dobj = device_objective(objective, dim)
+    _lib.check(lib.apo_run_updates_scripted(
+        _lib.ptr(snap_pos), _lib.ptr(snap_fit), _lib.ptr(in_dr), _lib.ptr(out_pos), _lib.ptr(out_fit), _lib.ptr(acc),
+        None, ps, dim, _lib.ptr(header), cfg.neighbor_pairs, cfg.bounds.lower, cfg.bounds.upper, cfg.eps, p_ah,
+        f_mult, decay, dobj.ref, _lib.ptr(p_dr_device(ps, dev)), _lib.ptr(warn), stream), "apo_run_updates_scripted")
+    m = miss.cpu().numpy().view(np.uint64)
+    if m[0]:
+        raise LookupError(f"unscripted draw at (individual {int(m[1])}, counter {int(m[2])})")
+    return out_pos, out_fit, acc.bool(), int(warn.item())

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(lib, name), name
     assert set(_lib.PROTOTYPES) >= set(_declared())
-    assert lib.apo_abi_version() == 3
+    assert lib.apo_abi_version() == 4
 
 
 def test_library_is_sm100a():
