@@ -1679,6 +1679,8 @@ int apo_run_batch_shaped(int64_t nruns, const uint64_t* seeds, const apo_objecti
     A.lpp = env_lpp && npairs == 1 ? 1 : 0;
     static const int env_lpp_g = getenv("APO_BATCH_LPP_G") ? atoi(getenv("APO_BATCH_LPP_G")) : 32;
     A.lpp_group = env_lpp_g;
+    static const int env_g = getenv("APO_BATCH_G") ? atoi(getenv("APO_BATCH_G")) : 0;
+    A.group = env_g;
     batch_smem_needs(objectives_host, nruns, dim, &A.cec_bufs, &A.tab_smem);
     BatchLayout L = batch_layout(A.ps, A.dim, A.ld, kWarps, A.cec_bufs, A.tab_smem);
     APO_CHECK((int64_t)L.total + 2048 <= smem_optin(), "population too large for the shared-memory batch kernel");

@@ -197,6 +197,7 @@ struct BatchArgs {
     unsigned* run_counter;
     int lpp;        // npairs == 1: lane-per-protozoon groups at dim <= kLppMaxDim (update_group_lpp)
     int lpp_group;  // protozoa per warp on that path
+    int group;      // minimum protozoa per warp on the warp-per-protozoon path (0: spread over all warps)
 };
 
 struct BatchLayout {
@@ -321,7 +322,7 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
     unsigned warn_total = 0;
     int cur = 0;
 #ifdef APO_BATCH_CLOCK
-    long long clk_sum[6] = {0, 0, 0, 0, 0, 0};
+    long long clk_sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long clk_prev = clock64();
 #define CLK(k)                                       \
     do {                                             \
@@ -350,28 +351,41 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
             const int count = (int)ceil((double)ps * pf);
             build_mask(ps, count, cbase, 1, cs, lane);
         };
+#ifdef APO_BATCH_CLOCK
+        const long long own_s0 = clock64();
         if (dr_overlap && warp == dr_warp) coordinator();
+        if (dr_overlap && warp == dr_warp) clk_sum[6] += clock64() - own_s0;
+#else
+        if (dr_overlap && warp == dr_warp) coordinator();
+#endif
         const int span = dr_overlap ? 32 * dr_warp : (int)blockDim.x;
-        int S = 1;
-        while (APO_BATCH_OVERLAP && S < 8 && 2 * S * ps <= span) S <<= 1;
+        int lgS = 0;
+        while (APO_BATCH_OVERLAP && lgS < 3 && (2 << lgS) * ps <= span) lgS++;
+        const int S = 1 << lgS;
         for (int base_t = 0; base_t < ps * S; base_t += span) {
             const int tt = base_t + (int)threadIdx.x;
             int cnt = 0;
-            int sl = tt / S;
+            const int sl = tt >> lgS;
             const bool act = (int)threadIdx.x < span && sl < ps;
             if (act) {
+                // branch-free count of (key, previous rank) pairs below this one (both loads always issued)
                 const unsigned long long k = keys[sl];
                 const int pr = rankof[sl];
-                for (int q = tt % S; q < ps; q += S) {
+#pragma unroll 4
+                for (int q = tt & (S - 1); q < ps; q += S) {
                     const unsigned long long kq = keys[q];
-                    cnt += (kq < k) || (kq == k && rankof[q] < pr);
+                    const int rq = rankof[q];
+                    cnt += (int)((kq < k) | ((kq == k) & (rq < pr)));
                 }
             }
             if ((int)threadIdx.x < span) {  // whole warps: span is a multiple of 32 and S divides 32
                 for (int o = 1; o < S; o <<= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
-                if (act && tt % S == 0) newrank[sl] = cnt;
+                if (act && (tt & (S - 1)) == 0) newrank[sl] = cnt;
             }
         }
+#ifdef APO_BATCH_CLOCK
+        if (!(dr_overlap && warp == dr_warp)) clk_sum[7] += clock64() - own_s0;
+#endif
         __syncthreads();
         CLK(0);
         for (int sl = threadIdx.x; sl < ps; sl += blockDim.x) {
@@ -405,7 +419,7 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
             const OrderedSlots R{pos[cur], fit[cur], order, ld};
             const bool lpp = MAXC == 1 && A.lpp && O.code < OBJ_CEC_BASE && dim <= kLppMaxDim;
             const int G = lpp ? min(32, max(A.lpp_group, (ps + nwarps - 1) / nwarps))
-                              : min(32, (ps + nwarps - 1) / nwarps);
+                              : min(32, max(A.group, (ps + nwarps - 1) / nwarps));
 #ifdef APO_BATCH_CLOCK
             const long long own0 = clock64();
 #endif
@@ -466,9 +480,10 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
     }
 #ifdef APO_BATCH_CLOCK
     if (threadIdx.x == 0 || threadIdx.x == 32 * (nwarps - 1))
-        printf("batch clock run %d thread %d: sort %lld order+dr %lld update %lld reduce %lld tail %lld own-update %lld (cycles/iter)\n",
+        printf("batch clock run %d thread %d: sort %lld order+dr %lld update %lld reduce %lld tail %lld own-update %lld own-coord %lld own-sort %lld (cycles/iter)\n",
                run, (int)threadIdx.x, clk_sum[0] / A.n_iters, clk_sum[1] / A.n_iters, clk_sum[2] / A.n_iters,
-               clk_sum[3] / A.n_iters, clk_sum[4] / A.n_iters, clk_sum[5] / A.n_iters);
+               clk_sum[3] / A.n_iters, clk_sum[4] / A.n_iters, clk_sum[5] / A.n_iters, clk_sum[6] / A.n_iters,
+               clk_sum[7] / A.n_iters);
     if (threadIdx.x == 0)
         printf("lpp warp 0 (cycles/iter): phaseA %llu cand+fold %llu select %llu\n", g_lpp_clk[0] / A.n_iters,
                g_lpp_clk[1] / A.n_iters, g_lpp_clk[3] / A.n_iters);
