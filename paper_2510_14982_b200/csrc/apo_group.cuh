@@ -639,22 +639,24 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
     }
     __syncwarp();
     const bool staging = g.ring != nullptr;
-    // TMA prefetch of member p's rows into ring stage p % kStages (lane 0 issues).
+    // TMA prefetch of member p's rows into ring stage p % kStages: lane r < 4 copies ring row r (own,
+    // partner, km, kp) when the operation reads it, so the warp issues one address computation and one
+    // bulk copy instead of four in sequence; lane 0 posts the byte count first.
     auto issue = [&](int p) {
-        if (lane == 0) {
+        if (lane < 4) {
             const int op = g.op[p];
             const int nrows = op == OP_AUTOTROPH ? 4 : op == OP_HETEROTROPH ? 3 : op == OP_REPRODUCTION ? 1 : 0;
             const int st = p % kStages;
-            double* dst = g.ring + (size_t)st * 4 * g.rld;
             const unsigned bytes = (unsigned)(8 * P.ld);
-            fence_proxy_async();
-            mbar_expect_tx(&g.bar[st], bytes * (unsigned)nrows);
-            const int* sl = g.slot + 4 * p;
-            if (nrows >= 1) bulk_g2s(dst, R.at_key(sl[0]), bytes, &g.bar[st]);
-            if (nrows == 4) bulk_g2s(dst + g.rld, R.at_key(sl[1]), bytes, &g.bar[st]);
-            if (nrows >= 3) {
-                bulk_g2s(dst + 2 * g.rld, R.at_key(sl[2]), bytes, &g.bar[st]);
-                bulk_g2s(dst + 3 * g.rld, R.at_key(sl[3]), bytes, &g.bar[st]);
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&g.bar[st], bytes * (unsigned)nrows);
+            }
+            __syncwarp(0xFu);
+            const bool mine = lane == 0 ? nrows >= 1 : lane == 1 ? nrows == 4 : nrows >= 3;
+            if (mine) {
+                fence_proxy_async();
+                bulk_g2s(g.ring + (size_t)(st * 4 + lane) * g.rld, R.at_key(g.slot[4 * p + lane]), bytes, &g.bar[st]);
             }
         }
     };
