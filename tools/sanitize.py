@@ -54,5 +54,16 @@ pz.run_batch(scfg, ["cec2022_f1"] * 4, list(range(4)), threads_per_run=64)      
 img = (np.arange(64 * 64) % 251).astype(np.uint8).reshape(64, 64)
 pz.apo_multithreshold(img, 3, "kapur", ps=40, iterations=5)
 pz.run(pz.ApoConfig(ps=64, dim=8, bounds=pz.Bounds(-5.0, 5.0, 8), max_iterations=5, rng="philox"), "cec2022_f4")
+# round 2, later: lane-per-protozoon batch groups (D <= 8) and scripted draws (APO_RNG_TABLE kernels)
+pz.run_batch(pz.ApoConfig(ps=100, dim=5, bounds=pz.Bounds(-5.0, 5.0, 5), max_iterations=4),
+             ["rosenbrock", "griewank", "sphere"] * 3, list(range(9)))
+from paper_2510_14982_b200.rng import COORDINATOR_INDEX, DrawTable  # noqa: E402
+
+tcfg = pz.ApoConfig(ps=64, dim=10, bounds=pz.Bounds(-5.0, 5.0, 10), max_iterations=5, seed=3)
+counters = list(range(6)) + [8 + d for d in range(10)] + [(1 << 32) + j for j in range(10)] + [1 << 33, (1 << 33) + 1]
+table = DrawTable.from_stream(3, 2, range(1, 65), counters)
+table.scalars.update(DrawTable.from_stream(3, 2, [COORDINATOR_INDEX], range(0, 65)).scalars)
+for name in ("rosenbrock", "cec2022_f6"):
+    pz.step(pz.initialize(tcfg, name), tcfg, name, 1, draws=table)
 torch.cuda.synchronize()
 print("sanitize exercise done")
