@@ -107,6 +107,9 @@ typedef struct apo_objective {
 #define APO_OBJ_FMA_SMALL_D 1
 
 int apo_abi_version(void);
+/* Largest `dim` the update / initialise / evaluate / run entries accept on this device (one warp's
+ * shared-memory scratch must fit a CTA: 6403 on a B200).  Needs a device. */
+int64_t apo_max_dim(void);
 const char *apo_last_error(void);
 /* Number of visible CUDA devices (cuda backend max_workers()). */
 int apo_device_count(void);

@@ -123,6 +123,7 @@ class apo_objective(C.Structure):
 
 PROTOTYPES = {
     "apo_abi_version": (_INT, []),
+    "apo_max_dim": (_I, []),
     "apo_last_error": (C.c_char_p, []),
     "apo_device_count": (_INT, []),
     "apo_run_updates": (_INT, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _U, _U, _I, _D, _D, _D, _D, _D, _D, _D, _I, _P,

@@ -91,6 +91,20 @@ int num_sms() {
 }
 
 // Warps per CTA for a given dim so the per-warp scratch fits comfortably.
+// Largest dimension the update, initialise and evaluate kernels take: ONE warp's warp-path scratch
+// (candidate, terms and auxiliary rows, permutation) must fit a CTA's opt-in shared memory
+// (6403 on a B200's 227 KB).
+int smem_optin();
+int64_t max_dim_supported() {
+    static int64_t m = 0;
+    if (m == 0) {
+        int64_t d = 8192;
+        while (d > 1 && warp_scratch_bytes((int)d) + 1024 > (size_t)smem_optin()) d--;
+        m = d;
+    }
+    return m;
+}
+
 int warps_for_dim(int64_t dim) {
     size_t per = warp_scratch_bytes((int)dim);
     int w = kWarps;
@@ -676,6 +690,8 @@ struct apo_run {
 
 extern "C" {
 
+int64_t apo_max_dim(void) { return max_dim_supported(); }
+
 int apo_abi_version(void) { return 4; }  // 4: scripted draws; 3: apo_objective.flags, apo_run_updates_ordered; 2: rng, shard/load/threshold
 
 const char* apo_last_error(void) { return g_err.c_str(); }
@@ -738,7 +754,7 @@ int updates_range(const double* positions, const double* fitness, const int32_t*
                   unsigned long long* warn_count, int64_t rank_lo, int64_t rank_hi, void* stream, int rng) {
     APO_CHECK(ps >= 1 && ps < (1LL << 31), "ps out of range");
     APO_CHECK(0 <= rank_lo && rank_lo < rank_hi && rank_hi <= ps, "rank range must satisfy 0 <= lo < hi <= ps");
-    APO_CHECK(dim >= 1 && dim <= 8192, "dim out of range (1..8192)");
+    APO_CHECK(dim >= 1 && dim <= max_dim_supported(), "dim out of range (1..apo_max_dim())");
     APO_CHECK(npairs >= 1, "npairs must be >= 1");
     APO_CHECK(positions && fitness && in_dr && out_pos && out_fit && p_dr, "NULL buffer");
     APO_CHECK(out_pos != positions && out_fit != fitness, "outputs must not alias inputs");
@@ -817,7 +833,7 @@ int apo_run_updates(const double* positions, const double* fitness, const uint8_
 
 int apo_evaluate(const double* x, int64_t n, int64_t dim, int64_t ld, const apo_objective* objective_host, double* out,
                  void* stream) {
-    APO_CHECK(n >= 0 && dim >= 1 && dim <= 8192 && ld >= dim, "bad shape");
+    APO_CHECK(n >= 0 && dim >= 1 && dim <= max_dim_supported() && ld >= dim, "bad shape (dim > apo_max_dim()?)");
     if (int rc = check_objective(objective_host, dim)) return rc;
     if (n == 0) return APO_OK;
     const int w = warps_for_dim(dim);
@@ -833,7 +849,8 @@ int apo_evaluate(const double* x, int64_t n, int64_t dim, int64_t ld, const apo_
 
 int apo_initialize(uint64_t seed, int64_t ps, int64_t dim, int64_t ld, double lower, double span,
                    const apo_objective* objective_host, double* positions, double* fitness, void* stream) {
-    APO_CHECK(ps >= 1 && ps < (1LL << 31) && dim >= 1 && dim <= 8192 && ld >= dim, "bad shape");
+    APO_CHECK(ps >= 1 && ps < (1LL << 31) && dim >= 1 && dim <= max_dim_supported() && ld >= dim,
+              "bad shape (dim > apo_max_dim()?)");
     APO_CHECK(positions && fitness, "NULL buffer");
     if (int rc = check_objective(objective_host, dim)) return rc;
     const int w = warps_for_dim(dim);
@@ -990,7 +1007,7 @@ int apo_run_create(apo_run** out, int64_t ps, int64_t dim, int64_t max_iteration
                    const double* sched_host, const double* p_dr_host, int rng, void* stream) {
     APO_CHECK(rng == RNG_KEYED || rng == RNG_PHILOX, "rng must be APO_RNG_KEYED or APO_RNG_PHILOX");
     APO_CHECK(out != nullptr, "out is NULL");
-    APO_CHECK(ps >= 1 && ps < (1LL << 31) && dim >= 1 && dim <= 8192, "bad shape");
+    APO_CHECK(ps >= 1 && ps < (1LL << 31) && dim >= 1 && dim <= max_dim_supported(), "bad shape (dim > apo_max_dim()?)");
     APO_CHECK(max_iterations >= 0 && npairs >= 1 && pf_max > 0.0 && pf_max <= 1.0, "bad config");
     APO_CHECK(max_iterations == 0 || sched_host, "sched_host is NULL");
     APO_CHECK(p_dr_host, "p_dr_host is NULL");
