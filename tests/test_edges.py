@@ -100,3 +100,26 @@ def test_largest_dimension_warp_kernel():
         pz.step(pz.Population(np.zeros((4, d1)), np.zeros(4), iteration=0, fe_count=4), big, "sphere", 0)
     with pytest.raises(Exception, match="dim"):
         pz.initialize(big, "sphere")
+
+
+@pytest.mark.parametrize("npairs,dim", [(9, 10), (20, 40), (12, 300)])
+def test_many_neighbour_pairs(npairs, dim, monkeypatch):
+    """More neighbour pairs than the kernels cache (kMaxCachedPairs = 8): pairs k >= 8 are drawn on the
+    fly per dimension (numba_backend.py:200-240); runs on the batch and device paths and a step, bit-exact."""
+    import paper_2510_14982_b200 as pz
+    from paper_2510_14982_b200 import engine
+
+    ps = 50
+    cfg = pz.ApoConfig(ps=ps, dim=dim, bounds=pz.Bounds(-3.0, 7.0, dim), max_iterations=8, seed=21,
+                       neighbor_pairs=npairs)
+    want = oracle.run(ps=ps, dim=dim, max_iterations=8, seed=21, name="rosenbrock", lower=-3.0, upper=7.0,
+                      npairs=npairs, nthreads=8)
+    for limit in (engine.BATCH_PS_LIMIT, 0):
+        monkeypatch.setattr(engine, "BATCH_PS_LIMIT", limit)
+        res = pz.run(cfg, "rosenbrock")
+        assert np.array_equal(res.trace, want["trace"]) and np.array_equal(res.population.positions, want["positions"])
+    pop = pz.initialize(cfg, "rosenbrock")
+    got = pz.step(pop, cfg, "rosenbrock", 3)
+    pos, fit, nw, _ = oracle.step(pop.positions, pop.fitness, seed=21, iteration=3, max_iterations=8,
+                                  name="rosenbrock", lower=-3.0, upper=7.0, npairs=npairs)
+    assert np.array_equal(got.positions, pos) and np.array_equal(got.fitness, fit)

@@ -168,7 +168,7 @@ def test_unscripted_draw_raises_lookup_error():
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,ps,dim,npairs", [("rosenbrock", 64, 10, 1), ("griewank", 300, 40, 2),
                                                 ("sphere", 2000, 3, 1), ("cec2022_f6", 500, 20, 1),
-                                                ("hgbat", 97, 7, 3)])
+                                                ("hgbat", 97, 7, 3), ("sphere", 70, 300, 2)])
 def test_keyed_stream_as_a_table_steps_like_the_stream(name, ps, dim, npairs):
     """A table holding the keyed stream's own draws reproduces the keyed step bit for bit: the table
     lookup is the only thing that changes between the two runs (fused, basic-split and CEC2022 paths)."""
