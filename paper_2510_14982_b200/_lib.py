@@ -35,6 +35,17 @@ SOURCES = ["apo_kernels.cu", "apo_update_sel.cu", "apo_update_dense.cu", "apo_ba
 # CEC2022-only TUs (parity unpinned, checked at 1e-9 relative): FMA contraction allowed.  Every TU
 # on the reference's bit-exact path keeps --fmad=false.
 FMA_SOURCES = ("apo_cec_eval.cu", "apo_cec_gemm.cu")
+# Hot-kernel TUs compiled a second time with -DAPO_PHILOX_VARIANT: the default objects read the keyed
+# stream only (no Philox call site in their loops), these serve rng = "philox" runs.
+PHILOX_VARIANTS = ("apo_update_sel.cu", "apo_update_dense.cu", "apo_batch_m1.cu", "apo_batch_m2.cu", "apo_batch_m4.cu",
+                   "apo_batch_m0.cu", "apo_batch_warp.cu")
+
+
+def _units():
+    """(source, object name, extra nvcc flags) of every translation unit."""
+    units = [(src, src.replace(".cu", ".o"), []) for src in SOURCES]
+    units += [(src, src.replace(".cu", "_philox.o"), ["-DAPO_PHILOX_VARIANT"]) for src in PHILOX_VARIANTS]
+    return units
 
 _lock = threading.Lock()
 _lib = None
@@ -77,25 +88,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
         headers.append(os.path.join(INCLUDE, "apo_b200.h"))
         newest_header = max(os.path.getmtime(h) for h in headers)
 
-        def compile_one(src):
-            obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        def compile_one(unit):
+            src, oname, extra = unit
+            obj = os.path.join(objdir, oname)
             if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(
                     newest_header, os.path.getmtime(os.path.join(CSRC, src))):
                 return obj, subprocess.CompletedProcess([], 0, "", "")  # up to date (same flags)
             f = flags
             if src in FMA_SOURCES:  # no bit-exact reference there: let nvcc contract multiply-adds
                 f = ["--fmad=true" if x == "--fmad=false" else x for x in flags]
-            cmd = [nvcc(), *ARCH_FLAGS, *f, "-I", INCLUDE, "-I", CSRC, "-c", "-o", obj, os.path.join(CSRC, src)]
+            cmd = [nvcc(), *ARCH_FLAGS, *f, *extra, "-I", INCLUDE, "-I", CSRC, "-c", "-o", obj, os.path.join(CSRC, src)]
             if verbose:
                 print(" ".join(cmd), flush=True)
             t0 = time.time()
             proc = subprocess.run(cmd, capture_output=True, text=True)
             if verbose:
-                print(f"  {src}: {time.time() - t0:.0f} s", flush=True)
+                print(f"  {oname}: {time.time() - t0:.0f} s", flush=True)
             return obj, proc
 
-        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-            results = list(ex.map(compile_one, SOURCES))
+        units = _units()
+        with ThreadPoolExecutor(max_workers=len(units)) as ex:
+            results = list(ex.map(compile_one, units))
         for obj, proc in results:
             if proc.returncode != 0:
                 raise ApoError(f"nvcc failed for {obj} ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")

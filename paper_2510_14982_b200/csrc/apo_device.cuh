@@ -170,6 +170,9 @@ __device__ __forceinline__ double table_draw(uint64_t table, uint64_t individual
 // own instantiations in apo_update_scripted.cu: any table code in the keyed kernels, even on a branch
 // they never take, measured +1.5-9% on the C4 update (it shifts ptxas' register allocation).
 __host__ __device__ __forceinline__ double uniform(const Key& k, uint64_t counter) {
+#if defined(APO_RNG_KEYED_ONLY) && defined(__CUDA_ARCH__)
+    return uniform(k.a, counter);  // keyed builds: the hot kernels carry no Philox call site
+#endif
     if (k.mode == RNG_KEYED) return uniform(k.a, counter);
 #ifdef __CUDA_ARCH__
 #ifdef APO_RNG_TABLE_ENABLED

@@ -33,6 +33,11 @@
 
 using namespace apo;
 
+namespace apo_philox {  // apo_update_sel.cu / apo_update_dense.cu built with APO_PHILOX_VARIANT
+const void* pick_update_sel(int dim, bool cand_only, bool cec);
+const void* pick_update_dense(int dim, bool cand_only, bool cec);
+}
+
 static_assert(sizeof(apo_draw_table) == sizeof(DrawTable) && offsetof(apo_draw_table, miss) == offsetof(DrawTable, miss),
               "apo_draw_table (include/apo_b200.h) and DrawTable (apo_device.cuh) must share one layout");
 
@@ -410,9 +415,13 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     while (w > 1 && per_warp * (size_t)w + 1024 > (size_t)smem_optin()) w--;  // e.g. fused CEC at D ~ 150-256
     const size_t smem = per_warp * (size_t)w;
     const bool cec = a.O.code > APO_OBJ_CEC2022_BASE;
-    const void* fn = scripted   ? pick_update_scripted(dim, split || gemm || bsplit, cec)
-                     : sel_mode ? pick_update_sel(dim, split || gemm || bsplit, cec)
-                                : pick_update_dense(dim, split || gemm || bsplit, cec);
+    // the keyed builds carry no Philox call site; Philox runs (device loop, shards) take their own build
+    const bool co = split || gemm || bsplit;
+    const bool philox = a.P.rng == RNG_PHILOX;
+    const void* fn = scripted ? pick_update_scripted(dim, co, cec)
+                     : philox ? (sel_mode ? apo_philox::pick_update_sel(dim, co, cec)
+                                          : apo_philox::pick_update_dense(dim, co, cec))
+                              : (sel_mode ? pick_update_sel(dim, co, cec) : pick_update_dense(dim, co, cec));
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
@@ -1732,7 +1741,7 @@ int apo_run_batch_shaped(int64_t nruns, const uint64_t* seeds, const apo_objecti
             workers = 0;
         }
     }
-    const void* fn = pick_run_batch((int)dim);
+    const void* fn = pick_run_batch((int)dim, rng);
     if (int rc = set_smem(fn, L.total)) return rc;
     A.nruns = (int)nruns;
     A.run_order = nullptr;

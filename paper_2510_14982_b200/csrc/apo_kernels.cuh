@@ -920,7 +920,7 @@ const void* pick_update_sel(int dim, bool cand_only, bool cec);
 const void* pick_update_dense(int dim, bool cand_only, bool cec);
 const void* pick_update_scripted(int dim, bool cand_only, bool cec);  // apo_update_scripted.cu
 cudaError_t launch_dr_scripted(uint64_t table, int ps, int count, int* perm, uint8_t* in_dr, cudaStream_t st);
-const void* pick_run_batch(int dim);
+const void* pick_run_batch(int dim, int rng);
 // apo_prologue.cu: stable sort + Dr set as one launch for small populations (else the CUB prologue)
 bool prologue_small_fits(long long ps);
 cudaError_t launch_prologue_small(int ps, const double* fit, const int* order_in, int* order_out, int count,

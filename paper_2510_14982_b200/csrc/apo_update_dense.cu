@@ -1,5 +1,12 @@
 // apo_update_dense.cu -- instantiates the fused update kernels with SEL=false
 // (run_updates boundary: dense rank-ordered rows).
+// Built twice (paper_2510_14982_b200/_lib.py): keyed-stream kernels (APO_RNG_KEYED_ONLY: no Philox call
+// site in the hot loops) and, with APO_PHILOX_VARIANT, the Philox build for sharded runs (apo_philox).
+#ifdef APO_PHILOX_VARIANT
+#define apo apo_philox
+#else
+#define APO_RNG_KEYED_ONLY 1
+#endif
 #include "apo_kernels.cuh"
 
 namespace apo {
