@@ -143,7 +143,13 @@ __host__ __device__ __forceinline__ double philox_draw(uint64_t seed, uint32_t b
 }
 
 #ifdef __CUDA_ARCH__
+// Out of line where keyed draws dominate (a call site in the keyed loops is cheaper than 10 rounds
+// inlined); the Philox builds of the hot kernels (APO_PHILOX_VARIANT) inline it.
+#if defined(APO_PHILOX_VARIANT) && !defined(APO_PHILOX_CALL)
+__device__ __forceinline__ double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
+#else
 __device__ __noinline__ double philox_uniform(uint64_t seed, uint32_t b, uint32_t c, uint64_t counter) {
+#endif
     return philox_draw(seed, b, c, counter);
 }
 #ifdef APO_RNG_TABLE_ENABLED
