@@ -34,8 +34,8 @@
 using namespace apo;
 
 namespace apo_philox {  // apo_update_sel.cu / apo_update_dense.cu built with APO_PHILOX_VARIANT
-const void* pick_update_sel(int dim, bool cand_only, bool cec);
-const void* pick_update_dense(int dim, bool cand_only, bool cec);
+const void* pick_update_sel(int dim, bool cand_only, bool cec, bool many);
+const void* pick_update_dense(int dim, bool cand_only, bool cec, bool many);
 }
 
 static_assert(sizeof(apo_draw_table) == sizeof(DrawTable) && offsetof(apo_draw_table, miss) == offsetof(DrawTable, miss),
@@ -418,10 +418,11 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
     // the keyed builds carry no Philox call site; Philox runs (device loop, shards) take their own build
     const bool co = split || gemm || bsplit;
     const bool philox = a.P.rng == RNG_PHILOX;
-    const void* fn = scripted ? pick_update_scripted(dim, co, cec)
-                     : philox ? (sel_mode ? apo_philox::pick_update_sel(dim, co, cec)
-                                          : apo_philox::pick_update_dense(dim, co, cec))
-                              : (sel_mode ? pick_update_sel(dim, co, cec) : pick_update_dense(dim, co, cec));
+    const bool many = a.P.npairs > 1;
+    const void* fn = scripted ? pick_update_scripted(dim, co, cec, many)
+                     : philox ? (sel_mode ? apo_philox::pick_update_sel(dim, co, cec, many)
+                                          : apo_philox::pick_update_dense(dim, co, cec, many))
+                              : (sel_mode ? pick_update_sel(dim, co, cec, many) : pick_update_dense(dim, co, cec, many));
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
     APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));

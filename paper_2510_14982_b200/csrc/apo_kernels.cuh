@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) k_update(UpdArgs A) {
 #endif
 // KIND: KIND_ANY (every objective), KIND_BASIC (no CEC2022 code), KIND_CAND
 // (candidates only: the CEC2022 split, k_cec_eval finishes the update).
-template <bool SEL, int MAXC, int KIND>
+template <bool SEL, int MAXC, int KIND, int NP>
 __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group(UpdArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const IterParams& P = A.P;
@@ -154,17 +154,17 @@ __global__ void __launch_bounds__(kThreads, APO_GROUP_MIN_BLOCKS) k_update_group
         const int n = min(G, A.rank_hi - (i0 - 1));
         if constexpr (SEL) {
             const SelSlots R{A.pos0, A.pos1, A.sel, A.fit, A.order, P.ld};
-            update_group<MAXC, OUT_SEL, KIND>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
+            update_group<MAXC, OUT_SEL, KIND, NP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, nullptr, A.out_fit,
                                         true, nullptr, nullptr, A.sel_next, g, lane, my_min, my_warn, &ring_phase,
                                         A.cand_ok);
         } else if (A.order) {  // sharded: rows addressed through the rank->row order, outputs by rank
             const OrderedSlots R{A.pos, A.fit, A.order, P.ld};
-            update_group<MAXC, OUT_FIXUP, KIND>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
+            update_group<MAXC, OUT_FIXUP, KIND, NP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
                                           A.out_fit, false, A.out_acc, A.out_warn, nullptr, g, lane, my_min,
                                           my_warn, nullptr, A.cand_ok);
         } else {
             const DenseSlots R{A.pos, A.fit, P.ld};
-            update_group<MAXC, OUT_FIXUP, KIND>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
+            update_group<MAXC, OUT_FIXUP, KIND, NP>(P, A.O, R, i0, n, A.in_dr_bytes, A.in_dr_bits, A.p_dr, A.out_pos,
                                           A.out_fit, false, A.out_acc, A.out_warn, nullptr, g, lane, my_min,
                                           my_warn, nullptr, A.cand_ok);
         }
@@ -916,9 +916,9 @@ __host__ __device__ inline int gemm_kp(int dim) { return (dim + 15) & ~15; }
 __host__ __device__ inline int gemm_np(int dim) { return (dim + 63) & ~63; }
 
 // Kernel getters (defined in the instantiating TUs).
-const void* pick_update_sel(int dim, bool cand_only, bool cec);
-const void* pick_update_dense(int dim, bool cand_only, bool cec);
-const void* pick_update_scripted(int dim, bool cand_only, bool cec);  // apo_update_scripted.cu
+const void* pick_update_sel(int dim, bool cand_only, bool cec, bool many);
+const void* pick_update_dense(int dim, bool cand_only, bool cec, bool many);
+const void* pick_update_scripted(int dim, bool cand_only, bool cec, bool many);  // apo_update_scripted.cu
 cudaError_t launch_dr_scripted(uint64_t table, int ps, int count, int* perm, uint8_t* in_dr, cudaStream_t st);
 const void* pick_run_batch(int dim, int rng);
 // apo_prologue.cu: stable sort + Dr set as one launch for small populations (else the CUB prologue)

@@ -11,20 +11,25 @@
 namespace apo_scripted {
 
 // The same choice as pick_update_dense (apo_update_dense.cu).
-const void* pick(int dim, bool cand_only, bool cec) {
+template <int NP>
+const void* pick_np(int dim, bool cand_only, bool cec) {
     if (cand_only) {
-        if (dim <= 32) return (const void*)k_update_group<false, 1, KIND_CAND>;
-        if (dim <= 64) return (const void*)k_update_group<false, 2, KIND_CAND>;
-        if (dim <= 128) return (const void*)k_update_group<false, 4, KIND_CAND>;
-        if (dim <= kGroupMaxDim) return (const void*)k_update_group<false, 0, KIND_CAND>;
+        if (dim <= 32) return (const void*)k_update_group<false, 1, KIND_CAND, NP>;
+        if (dim <= 64) return (const void*)k_update_group<false, 2, KIND_CAND, NP>;
+        if (dim <= 128) return (const void*)k_update_group<false, 4, KIND_CAND, NP>;
+        if (dim <= kGroupMaxDim) return (const void*)k_update_group<false, 0, KIND_CAND, NP>;
         return (const void*)k_update<false>;
     }
     if (dim > kGroupMaxDim) return (const void*)k_update<false>;
-    if (cec) return (const void*)k_update_group<false, 0, KIND_ANY>;
-    if (dim <= 32) return (const void*)k_update_group<false, 1, KIND_BASIC>;
-    if (dim <= 64) return (const void*)k_update_group<false, 2, KIND_BASIC>;
-    if (dim <= 128) return (const void*)k_update_group<false, 4, KIND_BASIC>;
-    return (const void*)k_update_group<false, 0, KIND_ANY>;
+    if (cec) return (const void*)k_update_group<false, 0, KIND_ANY, NP>;
+    if (dim <= 32) return (const void*)k_update_group<false, 1, KIND_BASIC, NP>;
+    if (dim <= 64) return (const void*)k_update_group<false, 2, KIND_BASIC, NP>;
+    if (dim <= 128) return (const void*)k_update_group<false, 4, KIND_BASIC, NP>;
+    return (const void*)k_update_group<false, 0, KIND_ANY, NP>;
+}
+
+const void* pick(int dim, bool cand_only, bool cec, bool many) {  // many: npairs > 1
+    return many ? pick_np<2>(dim, cand_only, cec) : pick_np<1>(dim, cand_only, cec);
 }
 
 // The coordinator's set from scripted draws: the reference's partial Fisher-Yates over ranks 1..ps
@@ -49,7 +54,9 @@ __global__ void k_dr_scripted(int ps, int count, Key base, int* __restrict__ per
 
 namespace apo {
 
-const void* pick_update_scripted(int dim, bool cand_only, bool cec) { return apo_scripted::pick(dim, cand_only, cec); }
+const void* pick_update_scripted(int dim, bool cand_only, bool cec, bool many) {
+    return apo_scripted::pick(dim, cand_only, cec, many);
+}
 
 cudaError_t launch_dr_scripted(uint64_t table, int ps, int count, int* perm, uint8_t* in_dr, cudaStream_t st) {
     const apo_scripted::Key base = apo_scripted::stream_key(apo_scripted::RNG_TABLE, table, 0, apo_scripted::kCoordinator);

@@ -15,20 +15,25 @@ namespace apo {
 // cand_only: the CEC2022 split path (dim <= kCecEvalMaxDim).  Fused CEC2022
 // (no split available) always takes the generic MAXC = 0 kernel so the
 // register-resident variants carry no CEC code.
-const void* pick_update_sel(int dim, bool cand_only, bool cec) {
+template <int NP>
+const void* pick_update_sel_np(int dim, bool cand_only, bool cec) {
     if (cand_only) {
-        if (dim <= 32) return (const void*)k_update_group<true, 1, KIND_CAND>;
-        if (dim <= 64) return (const void*)k_update_group<true, 2, KIND_CAND>;
-        if (dim <= 128) return (const void*)k_update_group<true, 4, KIND_CAND>;
-        if (dim <= kGroupMaxDim) return (const void*)k_update_group<true, 0, KIND_CAND>;
+        if (dim <= 32) return (const void*)k_update_group<true, 1, KIND_CAND, NP>;
+        if (dim <= 64) return (const void*)k_update_group<true, 2, KIND_CAND, NP>;
+        if (dim <= 128) return (const void*)k_update_group<true, 4, KIND_CAND, NP>;
+        if (dim <= kGroupMaxDim) return (const void*)k_update_group<true, 0, KIND_CAND, NP>;
         return (const void*)k_update<true>;  // candidates-only through UpdArgs::cand_ok
     }
     if (dim > kGroupMaxDim) return (const void*)k_update<true>;
-    if (cec) return (const void*)k_update_group<true, 0, KIND_ANY>;
-    if (dim <= 32) return (const void*)k_update_group<true, 1, KIND_BASIC>;
-    if (dim <= 64) return (const void*)k_update_group<true, 2, KIND_BASIC>;
-    if (dim <= 128) return (const void*)k_update_group<true, 4, KIND_BASIC>;
-    return (const void*)k_update_group<true, 0, KIND_ANY>;
+    if (cec) return (const void*)k_update_group<true, 0, KIND_ANY, NP>;
+    if (dim <= 32) return (const void*)k_update_group<true, 1, KIND_BASIC, NP>;
+    if (dim <= 64) return (const void*)k_update_group<true, 2, KIND_BASIC, NP>;
+    if (dim <= 128) return (const void*)k_update_group<true, 4, KIND_BASIC, NP>;
+    return (const void*)k_update_group<true, 0, KIND_ANY, NP>;
+}
+
+const void* pick_update_sel(int dim, bool cand_only, bool cec, bool many) {  // many: npairs > 1
+    return many ? pick_update_sel_np<2>(dim, cand_only, cec) : pick_update_sel_np<1>(dim, cand_only, cec);
 }
 
 }  // namespace apo
