@@ -41,10 +41,16 @@ PHILOX_VARIANTS = ("apo_update_sel.cu", "apo_update_dense.cu", "apo_batch_m1.cu"
                    "apo_batch_m0.cu", "apo_batch_warp.cu")
 
 
+# Batch TUs compiled once more with -DAPO_MANY_PAIRS_VARIANT: keyed kernels for npairs > 1 (the default
+# objects are built for npairs == 1 only).
+MANY_PAIRS_VARIANTS = ("apo_batch_m1.cu", "apo_batch_m2.cu", "apo_batch_m4.cu", "apo_batch_m0.cu")
+
+
 def _units():
     """(source, object name, extra nvcc flags) of every translation unit."""
     units = [(src, src.replace(".cu", ".o"), []) for src in SOURCES]
     units += [(src, src.replace(".cu", "_philox.o"), ["-DAPO_PHILOX_VARIANT"]) for src in PHILOX_VARIANTS]
+    units += [(src, src.replace(".cu", "_many.o"), ["-DAPO_MANY_PAIRS_VARIANT"]) for src in MANY_PAIRS_VARIANTS]
     return units
 
 _lock = threading.Lock()

@@ -10,6 +10,13 @@ const void* batch_kernel_m0();
 const void* batch_kernel_warp();
 }  // namespace apo_philox
 
+namespace apo_many {  // keyed, npairs > 1 (APO_MANY_PAIRS_VARIANT)
+const void* batch_kernel_m1();
+const void* batch_kernel_m2();
+const void* batch_kernel_m4();
+const void* batch_kernel_m0();
+}  // namespace apo_many
+
 namespace apo {
 
 const void* batch_kernel_m1();
@@ -18,7 +25,13 @@ const void* batch_kernel_m4();
 const void* batch_kernel_m0();
 const void* batch_kernel_warp();
 
-const void* pick_run_batch(int dim, int rng) {
+const void* pick_run_batch(int dim, int rng, bool many) {
+    if (many && rng != RNG_PHILOX && dim <= kGroupMaxDim) {
+        if (dim <= 32) return apo_many::batch_kernel_m1();
+        if (dim <= 64) return apo_many::batch_kernel_m2();
+        if (dim <= 128) return apo_many::batch_kernel_m4();
+        return apo_many::batch_kernel_m0();
+    }
     if (rng == RNG_PHILOX) {
         if (dim <= 32) return apo_philox::batch_kernel_m1();
         if (dim <= 64) return apo_philox::batch_kernel_m2();

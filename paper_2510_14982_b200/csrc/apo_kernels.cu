@@ -1742,7 +1742,7 @@ int apo_run_batch_shaped(int64_t nruns, const uint64_t* seeds, const apo_objecti
             workers = 0;
         }
     }
-    const void* fn = pick_run_batch((int)dim, rng);
+    const void* fn = pick_run_batch((int)dim, rng, npairs > 1);
     if (int rc = set_smem(fn, L.total)) return rc;
     A.nruns = (int)nruns;
     A.run_order = nullptr;

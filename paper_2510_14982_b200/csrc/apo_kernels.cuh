@@ -249,7 +249,8 @@ constexpr int kBatchMaxThreads = 640;  // 96 registers: 5 warps per SM sub-parti
 #ifndef APO_BATCH_MAXNREG
 #define APO_BATCH_MAXNREG 96
 #endif
-template <int MAXC>
+// NP as in update_group: 1 / 2 = built for npairs == 1 / > 1 only (the keyed builds), 0 = either.
+template <int MAXC, int NP = 0>
 __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ unsigned long long red_min[32];
@@ -417,7 +418,7 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
         unsigned my_warn = 0;
         if constexpr (MAXC >= 0) {
             const OrderedSlots R{pos[cur], fit[cur], order, ld};
-            const bool lpp = MAXC == 1 && A.lpp && O.code < OBJ_CEC_BASE && dim <= kLppMaxDim;
+            const bool lpp = MAXC == 1 && NP != 2 && A.lpp && O.code < OBJ_CEC_BASE && dim <= kLppMaxDim;
             const int G = lpp ? min(32, max(A.lpp_group, (ps + nwarps - 1) / nwarps))
                               : min(32, max(A.group, (ps + nwarps - 1) / nwarps));
 #ifdef APO_BATCH_CLOCK
@@ -429,7 +430,7 @@ __global__ void __maxnreg__(APO_BATCH_MAXNREG) k_run_batch(BatchArgs A) {
                     update_group_lpp(P, O, R, i0, min(G, ps - q * G), cs.bits, A.p_dr, pos[nxt], fit[nxt], g, lane,
                                      my_min, my_warn);
                 else
-                    update_group<MAXC, OUT_FIXUP, KIND_ANY>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr,
+                    update_group<MAXC, OUT_FIXUP, KIND_ANY, NP>(P, O, R, i0, min(G, ps - q * G), nullptr, cs.bits, A.p_dr,
                                                             pos[nxt], fit[nxt], true, nullptr, nullptr, nullptr, g,
                                                             lane, my_min, my_warn);
             }
@@ -920,7 +921,7 @@ const void* pick_update_sel(int dim, bool cand_only, bool cec, bool many);
 const void* pick_update_dense(int dim, bool cand_only, bool cec, bool many);
 const void* pick_update_scripted(int dim, bool cand_only, bool cec, bool many);  // apo_update_scripted.cu
 cudaError_t launch_dr_scripted(uint64_t table, int ps, int count, int* perm, uint8_t* in_dr, cudaStream_t st);
-const void* pick_run_batch(int dim, int rng);
+const void* pick_run_batch(int dim, int rng, bool many);
 // apo_prologue.cu: stable sort + Dr set as one launch for small populations (else the CUB prologue)
 bool prologue_small_fits(long long ps);
 cudaError_t launch_prologue_small(int ps, const double* fit, const int* order_in, int* order_out, int count,
