@@ -26,8 +26,12 @@ def raw_metrics(path):
         i = h.index(name)
         v = float(vals[i].replace(",", ""))
         u = units[i]
-        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
-                    "msecond": 1e6, "second": 1e9}.get(u, 1)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+                 "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6,
+                 "s": 1e9, "%": 1, "": 1}
+        if u not in scale:
+            raise ValueError(f"unknown ncu unit {u!r} for {name}")
+        return v * scale[u]
 
     d = {"dram_bytes": get("dram__bytes_read.sum") + get("dram__bytes_write.sum"),
          "duration_ns": get("gpu__time_duration.sum")}
@@ -67,6 +71,8 @@ def main(specs):
         entry = {**m, "launch": f"{objective} ps=1e6 D=100 iteration {t} of T={T} (seed 0)", "report": os.path.basename(rep)}
         if key.startswith("c4:"):  # the candidate / update kernel: the algorithmic bytes of this launch
             entry["algorithmic_bytes"], entry["p_auto"] = algorithmic_bytes(objective, t, T)
+            entry["traffic_over_algorithmic"] = round(entry["dram_bytes"] / entry["algorithmic_bytes"], 4)
+            entry["algorithmic_gbs"] = round(entry["algorithmic_bytes"] / entry["duration_ns"], 1)
         launches[key] = entry
     doc = {"_source": "ncu --set full, one launch each (tools/traffic_update.py): dram__bytes_read.sum + "
                       "dram__bytes_write.sum, sm__pipe_tensor_subpipe_dmma_cycles_active; algorithmic bytes of the "
