@@ -42,6 +42,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// The same two on 32-bit shared-memory addresses computed once per kernel (the ring's hot path).
+__device__ __forceinline__ void mbar_expect_tx_s(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
@@ -93,13 +103,16 @@ struct GroupScratch {
     double* T;            // [batch][tstride] fitness terms
     double* ring;         // [kStages][4][rld] staged rows (nullptr if not staging)
     uint64_t* bar;        // [kStages] mbarriers of the ring
+    const double** rsrc;  // [32][4] global source of each ring row (staging; set before the first issue)
+    unsigned* rmask;      // [32] ring rows a member reads: bit r = row r (own, partner, km, kp)
     WarpScratch ws;       // only ws.pk / ws.pw (pair cache for npairs > 1) are used
     int dp, words, tstride, cstride, batch, rld;
 };
 
 __host__ __device__ inline int ring_ld(int dim) { return (dim + 1) & ~1; }
 __host__ __device__ inline size_t ring_bytes(int dim, bool stage) {
-    return stage ? (size_t)kStages * 4 * 8 * (size_t)ring_ld(dim) + 16 * kStages : 0;
+    // rows, mbarriers (16 B each), then the per-member row sources and masks
+    return stage ? (size_t)kStages * 4 * 8 * (size_t)ring_ld(dim) + 16 * kStages + 32 * 4 * 8 + 32 * 4 : 0;
 }
 
 // Layout: [header: scalars, slots, ops, pair cache, mask bits][union: phase-A
@@ -162,9 +175,13 @@ __device__ inline GroupScratch group_scratch(unsigned char* base, int dim, bool 
     if (stage) {
         g.ring = reinterpret_cast<double*>(base + group_head_bytes(dim) + group_union_bytes(dim, cec_bufs));
         g.bar = reinterpret_cast<uint64_t*>(g.ring + (size_t)kStages * 4 * g.rld);
+        g.rsrc = reinterpret_cast<const double**>(g.bar + 2 * kStages);
+        g.rmask = reinterpret_cast<unsigned*>(g.rsrc + 32 * 4);
     } else {
         g.ring = nullptr;
         g.bar = nullptr;
+        g.rsrc = nullptr;
+        g.rmask = nullptr;
     }
     g.ws.cand = g.ws.terms = nullptr;
     g.ws.head = g.ws.prev = g.ws.rj = nullptr;
@@ -645,25 +662,36 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
     // TMA prefetch of member p's rows into ring stage p % kStages: lane r < 4 copies ring row r (own,
     // partner, km, kp) when the operation reads it, so the warp issues one address computation and one
     // bulk copy instead of four in sequence; lane 0 posts the byte count first.
+    // The members' row sources and masks are resolved once, lane-parallel, before the first issue.
+    unsigned ring_s = 0, bar_s = 0;
     auto issue = [&](int p) {
         if (lane < 4) {
-            const int op = g.op[p];
-            const int nrows = op == OP_AUTOTROPH ? 4 : op == OP_HETEROTROPH ? 3 : op == OP_REPRODUCTION ? 1 : 0;
+            const unsigned m = g.rmask[p];
             const int st = p % kStages;
             const unsigned bytes = (unsigned)(8 * P.ld);
+            const unsigned bar = bar_s + 8u * (unsigned)st;
             if (lane == 0) {
                 fence_proxy_async();
-                mbar_expect_tx(&g.bar[st], bytes * (unsigned)nrows);
+                mbar_expect_tx_s(bar, bytes * (unsigned)__popc(m));
             }
             __syncwarp(0xFu);
-            const bool mine = lane == 0 ? nrows >= 1 : lane == 1 ? nrows == 4 : nrows >= 3;
-            if (mine) {
+            if ((m >> lane) & 1u) {
                 fence_proxy_async();
-                bulk_g2s(g.ring + (size_t)(st * 4 + lane) * g.rld, R.at_key(g.slot[4 * p + lane]), bytes, &g.bar[st]);
+                bulk_g2s_s(ring_s + 8u * (unsigned)((st * 4 + lane) * g.rld), g.rsrc[4 * p + lane], bytes, bar);
             }
         }
     };
     if (staging) {
+        ring_s = smem_u32(g.ring);
+        bar_s = smem_u32(g.bar);
+        if (lane < n) {
+            const int op = g.op[lane];
+            const unsigned m = op == OP_AUTOTROPH ? 0xFu : op == OP_HETEROTROPH ? 0xDu : op == OP_REPRODUCTION ? 0x1u : 0u;
+            g.rmask[lane] = m;
+            for (int r = 0; r < 4; r++)
+                if ((m >> r) & 1u) g.rsrc[4 * lane + r] = R.at_key(g.slot[4 * lane + r]);
+        }
+        __syncwarp();
         for (int p = 0; p < kStages && p < n; p++) issue(p);
     }
     const bool two = two_term_arrays(O.code);
