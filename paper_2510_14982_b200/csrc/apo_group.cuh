@@ -517,7 +517,9 @@ enum OutMode : int {
 enum GroupKind : int { KIND_ANY = 0, KIND_BASIC = 1, KIND_CAND = 2 };
 
 // XCOPY (with CO): the clamped candidate also goes to T1[d] (the fused CEC kernel's shared-memory tile).
-template <int MAXC, bool MANY, bool CO, class Rows, bool XCOPY = false>
+// VOTE = false: returns this lane's finiteness only (the caller folds the warp's votes for a whole
+// batch of members with one reduction instead of one vote per member).
+template <int MAXC, bool MANY, bool CO, class Rows, bool XCOPY = false, bool VOTE = true>
 __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, const Rows& R, int i, int p,
                                        double* cand_out, double* T1, double* T2, const GroupScratch& g, int lane,
                                        const double* staged) {
@@ -634,7 +636,8 @@ __device__ inline bool group_candidate(const IterParams& P, const ObjDesc& O, co
             finish(d, cv, d < dim);
         }
     }
-    return __all_sync(kFull, ok);
+    if constexpr (VOTE) return __all_sync(kFull, ok);
+    return ok;
 }
 
 // One group of n <= 32 consecutive ranks [i0, i0+n) on one warp.
@@ -705,7 +708,7 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
     double* T2base = g.T + (size_t)(g.batch / 2) * g.tstride;
     for (int h = 0; h < n; h += B) {
         const int nb = min(B, n - h);
-        unsigned okmask = 0;
+        unsigned badbits = 0;  // bit q: a non-finite candidate element of member h+q in this lane
         for (int q = 0; q < nb; q++) {
             const int p = h + q, i = i0 + p;
             const int own_key = g.slot[4 * p];
@@ -723,21 +726,25 @@ __device__ inline void update_group(const IterParams& P, const ObjDesc& O, const
             }
             bool ok;
             if constexpr (NP == 1) {
-                ok = group_candidate<MAXC, false, cand_only>(P, O, R, i, p, dst, T1, T2, g, lane, staged);
+                ok = group_candidate<MAXC, false, cand_only, Rows, false, false>(P, O, R, i, p, dst, T1, T2, g, lane,
+                                                                             staged);
             } else if constexpr (NP == 2) {
-                ok = group_candidate<MAXC, true, cand_only>(P, O, R, i, p, dst, T1, T2, g, lane, staged);
+                ok = group_candidate<MAXC, true, cand_only, Rows, false, false>(P, O, R, i, p, dst, T1, T2, g, lane,
+                                                                            staged);
             } else {
-                ok = P.npairs > 1
-                         ? group_candidate<MAXC, true, cand_only>(P, O, R, i, p, dst, T1, T2, g, lane, staged)
-                         : group_candidate<MAXC, false, cand_only>(P, O, R, i, p, dst, T1, T2, g, lane, staged);
+                ok = P.npairs > 1 ? group_candidate<MAXC, true, cand_only, Rows, false, false>(P, O, R, i, p, dst, T1,
+                                                                                              T2, g, lane, staged)
+                                  : group_candidate<MAXC, false, cand_only, Rows, false, false>(P, O, R, i, p, dst, T1,
+                                                                                               T2, g, lane, staged);
             }
-            okmask |= (ok ? 1u : 0u) << q;
+            badbits |= (ok ? 0u : 1u) << q;
             if (staging) {
                 __syncwarp();
                 if (p + kStages < n) issue(p + kStages);
             }
         }
         __syncwarp();
+        const unsigned okmask = ~__reduce_or_sync(kFull, badbits);
         if constexpr (cand_only) {
             if (lane < nb) {
                 const int own_key = g.slot[4 * (h + lane)];
