@@ -314,7 +314,10 @@ __device__ inline void group_phase_a(const IterParams& P, const Rows& R, int i, 
     for (int w = 0; w < g.words; w++) bits[w] = 0u;
     if (op != OP_DORMANCY && count > 0) {
         unsigned char* perm = g.perm + (size_t)lane * g.dp;
-        for (int d = 0; d < dim; d++) perm[d] = (unsigned char)d;
+        // identity, four entries per 32-bit store (rows are 4-byte aligned, dim <= 256); bytes past dim
+        // are never read
+        unsigned* perm4 = reinterpret_cast<unsigned*>(perm);
+        for (int w = 0; w < (dim + 3) >> 2; w++) perm4[w] = 0x03020100u + 0x04040404u * (unsigned)w;
         for (int j = 0; j < count; j++) {
             int r = j + (int)(uniform(base, kMaskBase + (uint64_t)j) * (double)(dim - j));
             if (r > dim - 1) r = dim - 1;
