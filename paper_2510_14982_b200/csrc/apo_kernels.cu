@@ -24,6 +24,9 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <utility>
 #include <vector>
@@ -117,10 +120,40 @@ int warps_for_dim(int64_t dim) {
     return w;
 }
 
+// Per-launch host work is cached per (kernel, device): cudaFuncSetAttribute only when a launch needs
+// more dynamic shared memory than already granted, occupancy queried once per launch shape (the
+// device loop at ps ~ 1e5 was host-bound on these calls).
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, size_t> g_smem_set;
+std::map<std::tuple<const void*, int, int, size_t>, int> g_occ;
+
 int set_smem(const void* fn, size_t bytes) {
-    // always: the 48 KB default covers static + dynamic shared memory, so a request just under 48 KB
-    // still fails to launch once the kernel's own static arrays are added (k_run_batch, ps = 48, D = 6)
-    if (bytes > 0) APO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    // always (the first time): the 48 KB default covers static + dynamic shared memory, so a request just
+    // under 48 KB still fails to launch once the kernel's own static arrays are added (k_run_batch,
+    // ps = 48, D = 6)
+    if (bytes == 0) return APO_OK;
+    int dev = 0;
+    APO_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t& have = g_smem_set[{fn, dev}];
+    if (have >= bytes) return APO_OK;
+    APO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+    return APO_OK;
+}
+
+int occupancy(int* per_sm, const void* fn, int threads, size_t smem) {
+    int dev = 0;
+    APO_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    const auto key = std::make_tuple(fn, dev, threads, smem);
+    auto it = g_occ.find(key);
+    if (it == g_occ.end()) {
+        int v = 0;
+        APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, threads, smem));
+        it = g_occ.emplace(key, v).first;
+    }
+    *per_sm = it->second;
     return APO_OK;
 }
 
@@ -425,7 +458,7 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
                               : (sel_mode ? pick_update_sel(dim, co, cec, many) : pick_update_dense(dim, co, cec, many));
     if (int rc = set_smem(fn, smem)) return rc;
     int per_sm = 1;
-    APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * w, smem));
+    if (int rc = occupancy(&per_sm, fn, 32 * w, smem)) return rc;
     if (per_sm < 1) per_sm = 1;
     if (a.rank_hi <= 0) a.rank_hi = a.P.ps;  // default: every rank
     const long long cap = (long long)per_sm * num_sms();
@@ -478,7 +511,7 @@ int launch_update(bool sel_mode, const UpdArgs& A0, cudaStream_t st, uint8_t* ca
         const size_t bsmem = direct ? 0 : kBasicEvalSmem;
         if (int rc = set_smem(fb, bsmem)) return rc;
         int bper = 1;
-        APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bper, fb, 32 * bw, bsmem));
+        if (int rc = occupancy(&bper, fb, 32 * bw, bsmem)) return rc;
         if (bper < 1) bper = 1;
         const long long groups = ((long long)B.n_rows + 31) / 32;
         const long long bneed = (groups + bw - 1) / bw;
@@ -580,7 +613,7 @@ int launch_cec_eval(bool sel_mode, const UpdArgs& a, cudaStream_t st, uint8_t* c
     }
     if (int rc = set_smem(fe, esmem)) return rc;
     int eper = 1;
-    APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&eper, fe, 32 * ewarps, esmem));
+    if (int rc = occupancy(&eper, fe, 32 * ewarps, esmem)) return rc;
     if (eper < 1) eper = 1;
     const long long tiles = ((long long)E.n_rows + kCecRows - 1) / kCecRows;
     const long long eneed = (tiles + ewarps - 1) / ewarps;
@@ -1097,7 +1130,7 @@ int apo_run_initialize(apo_run* r) {
     const size_t smem = warp_scratch_bytes((int)r->dim) * (size_t)w;
     if (int rc = set_smem((const void*)k_init, smem)) return rc;
     int per_sm = 1;
-    APO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_init, 32 * w, smem));
+    if (int rc = occupancy(&per_sm, (const void*)k_init, 32 * w, smem)) return rc;
     const long long need = (r->ps + w - 1) / w;
     const long long cap = (long long)(per_sm > 0 ? per_sm : 1) * num_sms();
     APO_CUDA(cudaMemsetAsync(r->trace_keys, 0xFF, 8 * (size_t)(r->T + 1), st));
