@@ -667,6 +667,19 @@ __global__ void __launch_bounds__(512, 1) k_cec_eval(CecEvalArgs A) {
             cp_async_commit();
             tile_next = tile_nxt;  // claimed one tile ahead
             sel_cur = sel_nxt;
+#ifndef APO_CEC_L2_PREFETCH
+#define APO_CEC_L2_PREFETCH 1
+#endif
+            if (APO_CEC_L2_PREFETCH && SEL && !A.init && lane < kCecRows && tile_next < ntiles) {
+                // the next tile's candidate rows into L2 while this one evaluates (one bulk prefetch per
+                // row; SEL rows have an even stride, so 8 * ld bytes is a multiple of 16)
+                const int rn = A.row0 + tile_next * kCecRows + lane;
+                if (rn < A.row0 + A.n_rows) {
+                    const double* src = (A.sel[rn] ? A.pos0 : A.pos1) + (size_t)rn * A.ld;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((unsigned)(8 * A.ld))
+                                 : "memory");
+                }
+            }
             cp_async_wait_all();
         }
         // the claim after next: issued now, read after the evaluation (its latency hides behind it)
