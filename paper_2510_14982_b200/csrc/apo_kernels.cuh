@@ -815,6 +815,10 @@ __device__ __forceinline__ void basic_select(const BasicEvalArgs& A, int g0, int
 // (a warp instruction touches 32 rows, the second half of each 32-byte sector follows from L1) and folds
 // it in registers; small enough to run 48 warps per SM, so the row streams of many warps overlap.
 constexpr int kBasicDirectWarps = 8;
+#ifndef APO_BASIC_UNROLL
+#define APO_BASIC_UNROLL 4
+#endif
+constexpr int kBasicUnroll = APO_BASIC_UNROLL;  // 16-byte loads in flight per lane
 template <bool SEL>
 __global__ void __launch_bounds__(32 * kBasicDirectWarps) k_basic_eval_direct(BasicEvalArgs A) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -834,7 +838,7 @@ __global__ void __launch_bounds__(32 * kBasicDirectWarps) k_basic_eval_direct(Ba
             const double* row = SEL ? (cur ? A.pos0 : A.pos1) + (size_t)r * A.ld : A.out_pos + (size_t)r * A.ld;
             const double2* row2 = reinterpret_cast<const double2*>(row);
             const int h = dim >> 1;
-#pragma unroll 4
+#pragma unroll kBasicUnroll
             for (int k = 0; k < h; k++) {
                 const double2 v = __ldcs(row2 + k);  // streamed once: evict-first
                 f.add(code, A.O.table, 2 * k, v.x);
